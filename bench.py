@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""S-MNN hot-path benchmark (driver contract).
+
+A *step* = one fused forward (smnn_factor_solve_fwd: assemble + block
+Cholesky + substitution) plus one fused backward (smnn_solve_bwd: dl/dbeta =
+M^{-1} dl/dy and the chained gradients) over one batch of synthetic instances
+already resident in HBM.  Metric: instance*timesteps per second, fwd+bwd.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload lorenz]
+                  [--dtype f32|f64|f32c64] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank solves its own full batch
+of independent instances (weak scaling, no data-path collective); the timed
+region is bracketed by barrier + synchronize and the max over ranks is taken.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth.workloads import WORKLOADS, make_grad_y, make_workload_inputs  # noqa: E402
+
+METRIC = "instance*timesteps/s fwd+bwd"
+UNIT = "instance*timesteps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="lorenz", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64", "f32c64"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--threads-per-inst", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers --
+
+def algorithmic_bytes(b: int, es: int):
+    """Unavoidable HBM bytes per instance*timestep.
+
+    fwd reads c (b), d, s and writes y (b): (2b + 2) elements;
+    bwd reads c (b), d, s, y (b), dl/dy (b) and writes dc (b), dd, ds: (4b + 4).
+    """
+    return (2 * b + 2) * es, (4 * b + 4) * es
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "hw_power_brake_slowdown": 0x80}
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+             0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+             0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def result(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        names = [n for bit, n in self.NAMES.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def cpu_baseline(x, gy, wl, budget_s=10.0):
+    """The fp64 oracle (banded tier) as it stands, on a bounded sample of instances."""
+    import oracle as O
+
+    n_total = x["coeffs"].shape[0]
+    order = np.random.default_rng(0).permutation(n_total)
+    done, t0 = 0, time.perf_counter()
+    while done < n_total:
+        i = order[done:done + 4]
+        args = (x["coeffs"][i], x["rhs"][i], x["iv"][i], x["steps"][i])
+        y = O.solve_instances(*args)
+        O.grads_instances(*args, gy[i], y=y)
+        done += len(i)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done * wl.T / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
+            "sample": f"{done} of {n_total} instances x T={wl.T} (fp64 banded LAPACK solve + adjoint grads), "
+                      f"{dt:.1f} s"}
+
+
+# ------------------------------------------------------------ reference ---
+
+def run_reference(args, wl):
+    """--impl reference: the oracle (fp64 CPU) timed per step on a bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+
+    n_sample = 8
+    x = make_workload_inputs(wl.with_(dtype="f64"), seed=1, n_inst=n_sample)
+    gy = make_grad_y(n_sample, wl.T, wl.order, dtype="f64", seed=2)
+    a = (x["coeffs"], x["rhs"], x["iv"], x["steps"])
+    for _ in range(args.warmup):
+        O.grads_instances(*a, gy, y=O.solve_instances(*a))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.grads_instances(*a, gy, y=O.solve_instances(*a))
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = n_sample * wl.T / (ms / 1e3)
+    cores = torch.get_num_threads()
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl.name, "desc": wl.desc, "B": wl.B, "D": wl.D, "T": wl.T, "order": wl.order,
+                   "sample_instances_per_step": n_sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{n_sample} instances x T={wl.T} per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ----------------------------------------------------------------- ours ----
+
+def main():
+    args = parse()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+        return
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (the S-MNN path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2410_06074_b200 as smnn
+
+    store = "f64" if args.dtype == "f64" else "f32"
+    compute = "f64" if args.dtype == "f32c64" else None
+    tdtype = torch.float64 if store == "f64" else torch.float32
+    es = 8 if store == "f64" else 4
+    b = wl.order + 1
+    # weak scaling: each rank owns a full batch of independent instances
+    x = make_workload_inputs(wl.with_(dtype=store), seed=1 + rank)
+    gy_np = make_grad_y(wl.n_inst, wl.T, wl.order, dtype=store, seed=100 + rank)
+    t = {k: torch.from_numpy(v).to(dev) for k, v in x.items()}
+    gy = torch.from_numpy(gy_np).to(dev)
+    w = smnn.Weights()
+    tpi = args.threads_per_inst
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi)
+        g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, w, compute, tpi)
+        return y, info, g
+
+    for _ in range(args.warmup):
+        y, info, g = step()
+    torch.cuda.synchronize()
+    assert int(info.abs().max()) == 0 and int(g[4].abs().max()) == 0, "numerical breakdown in warm-up"
+
+    stream = torch.cuda.current_stream(dev)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # evict L2 between timed steps (outside the events)
+            ev[i][0].record(stream)
+            y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi)
+            ev[i][1].record(stream)
+            g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, w, compute, tpi)
+            ev[i][2].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    tot_ms = float(np.sum(fwd_ms) + np.sum(bwd_ms))
+    if dist:
+        tt = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot_ms = float(tt.item())
+    ms_per_step = tot_ms / args.steps
+    units = wl.n_inst * wl.T * world
+    value = units / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (algorithmic bytes / measured launch time)
+    fb, bb = algorithmic_bytes(b, es)
+    f_avg, b_avg = float(np.mean(fwd_ms)), float(np.mean(bwd_ms))
+    inst_steps = wl.n_inst * wl.T
+    peak, peak_kind = measured_peaks()
+    kern = "smnn_solve_bwd" if b_avg >= f_avg else "smnn_factor_solve_fwd"
+    kbytes = inst_steps * (bb if b_avg >= f_avg else fb)
+    kms = max(b_avg, f_avg)
+    achieved = kbytes / (kms / 1e3) / 1e9
+    step_gbs = inst_steps * (fb + bb) / (ms_per_step / 1e3) / 1e9
+
+    # end-to-end through the host-buffer C-ABI plan (H2D + fwd + bwd + D2H)
+    e2e = None
+    if args.e2e_steps > 0:
+        plan = smnn.HostPlan(wl.n_inst, wl.T, wl.order, wl.n_iv, tdtype, w, compute, dev)
+        h = {k: torch.from_numpy(v).pin_memory() for k, v in x.items()}
+        hg = torch.from_numpy(gy_np).pin_memory()
+        outs = [torch.empty_like(h["coeffs"]).pin_memory(), torch.empty_like(h["coeffs"]).pin_memory(),
+                torch.empty_like(h["rhs"]).pin_memory(), torch.empty_like(h["iv"]).pin_memory(),
+                torch.empty_like(h["steps"]).pin_memory()]
+        plan.fwd_bwd(h["coeffs"], h["rhs"], h["iv"], h["steps"], hg, *outs)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            plan.fwd_bwd(h["coeffs"], h["rhs"], h["iv"], h["steps"], hg, *outs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        plan.close()
+        h2d = sum(v.nbytes for v in x.values()) + gy_np.nbytes
+        d2h = sum(o.numel() * o.element_size() for o in outs)
+        e2e = {"value": units / (ems / args.e2e_steps / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        x64 = {k: v.astype(np.float64) for k, v in x.items()}
+        cpu = cpu_baseline(x64, gy_np.astype(np.float64), wl)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if args.dtype in ("f64", "f32c64") else "f32",
+            "data": "synthetic (seeded, synth/workloads.py recipe)",
+            "config": {"workload": wl.name, "desc": wl.desc, "B": wl.B, "D": wl.D, "T": wl.T, "order": wl.order,
+                       "instances_per_gpu": wl.n_inst, "storage": store, "arithmetic": "f64" if compute or
+                       store == "f64" else "f32", "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"dp{world} (instances sharded, no data-path collective)",
+                       "threads_per_inst": tpi or "auto"},
+            "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": kbytes, "launch_ms": kms,
+                         "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
+            "kernels_ms": {"smnn_factor_solve_fwd": f_avg, "smnn_solve_bwd": b_avg},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.result(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

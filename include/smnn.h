@@ -1,0 +1,147 @@
+/*
+ * smnn.h -- C ABI of the B200-native S-MNN hot path (arXiv 2410.06074).
+ *
+ * One *instance* is one (batch, ODE-dim) pair of the paper's linear ODE
+ * (PAPER.md:68-80 with V = Q = 1): a single variable y of derivative order
+ * R = `order`, T time points, initial values at the first time point only
+ * (T_init = 1, R_init = n_iv - 1).  Instances are
+ * independent; a call processes `n_inst` = B*D of them.
+ *
+ * Tensor layouts (row-major, instance outermost, "paper layout" of
+ * BASELINE.json north_star; b = R + 1 is the block size of PAPER.md:158):
+ *   coeffs [n_inst, T, b]     c_{t,r}  of sum_r c_{t,r} y^{(r)}_t = d_t
+ *   rhs    [n_inst, T]        d_t
+ *   iv     [n_inst, n_iv]     u_r, r < n_iv, at t = 0
+ *   steps  [n_inst, T-1]      s_t = span between t and t+1, > 0
+ *   y      [n_inst, T, b]     y_{t,r}, the solution of Eq. least_squares
+ *   grad_* same shape as the tensor they differentiate.
+ *   M_diag [n_inst, T, b, b]  M_t = M_{t,t}        (App. A.1 :625-634)
+ *   N_sub  [n_inst, T-1, b, b] N_t = M_{t+1,t}     (lower off-diagonal block)
+ *   beta   [n_inst, T, b]     beta_t
+ *   L      [n_inst, T, b, b]  lower-triangular Cholesky blocks, zeros above the diagonal
+ *   P      [n_inst, T-1, b, b] LDL multipliers, P L L^T P^T = M
+ *
+ * Element type: `dtype` selects storage and arithmetic:
+ *   SMNN_F32      float storage, float arithmetic
+ *   SMNN_F64      double storage, double arithmetic
+ *   SMNN_F32_C64  float storage, double arithmetic (fp32 HBM traffic,
+ *                 fp64-accurate normal equations)
+ *
+ * Memory: unless stated otherwise every pointer is a DEVICE pointer on the
+ * current CUDA device, owned by the caller, not retained after the call;
+ * inputs are read-only, outputs are fully overwritten.  Calls are
+ * asynchronous on `stream` (a cudaStream_t, NULL = legacy default stream).
+ *
+ * Errors: every entry point returns SMNN_OK (0) or a negative code; the
+ * message of the last failure on the calling thread is returned by
+ * smnn_last_error().  Argument errors are detected before any launch.
+ * Numerical breakdown (a non-positive or non-finite Cholesky pivot, i.e.
+ * M not numerically SPD) is reported per instance in `info` (may be NULL):
+ * info[i] = 0 on success, else 1 + the time index of the first failing
+ * block (like LAPACK potrf); the outputs of such an instance are undefined.
+ */
+#ifndef SMNN_H_
+#define SMNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMNN_F32 0
+#define SMNN_F64 1
+#define SMNN_F32_C64 2
+
+#define SMNN_OK 0
+#define SMNN_ERR_ARG (-1)         /* invalid argument / shape / null pointer      */
+#define SMNN_ERR_CUDA (-2)        /* a CUDA runtime call or launch failed        */
+#define SMNN_ERR_UNSUPPORTED (-3) /* order > 3, or dtype unknown                 */
+#define SMNN_ERR_WORKSPACE (-4)   /* workspace_bytes < smnn_workspace_bytes()    */
+
+#define SMNN_MAX_ORDER 3
+
+typedef struct smnn_problem {
+  int64_t n_inst;   /* number of independent instances (B*D), >= 1              */
+  int32_t T;        /* time points per instance, >= 1                            */
+  int32_t order;    /* R in 0..3; block size b = R + 1                           */
+  int32_t n_iv;     /* initial values per instance, 1..R+1 (R_init = n_iv - 1)   */
+  int32_t dtype;    /* SMNN_F32 | SMNN_F64 | SMNN_F32_C64                        */
+  int32_t threads_per_inst; /* time-chunks (= CUDA threads) per instance; 0 = auto */
+  int32_t reserved; /* must be 0                                                 */
+  double w_gov;     /* importance weights of PAPER.md:130, all > 0               */
+  double w_init;
+  double w_smooth;
+} smnn_problem;
+
+/* Library identification and the last error message of this thread. */
+const char* smnn_version(void);
+const char* smnn_last_error(void);
+
+/* Bytes of device workspace the fused kernels need for `p` on the current
+ * device (checkpoint scratch of the time-parallel solver, one slot per
+ * resident CTA).  Pass at least this much to smnn_factor_solve_fwd /
+ * smnn_solve_bwd.  Returns 0 and sets the error on invalid `p`. */
+size_t smnn_workspace_bytes(const smnn_problem* p);
+
+/* Appendix A.1: assemble the non-zero blocks of
+ * M = A^T W A and beta = A^T W b for every instance.  Outputs M_diag, N_sub,
+ * beta in the storage type of `dtype`.  N_sub may be NULL when T == 1. */
+int smnn_assemble(const smnn_problem* p, const void* coeffs, const void* rhs,
+                  const void* iv, const void* steps, void* M_diag, void* N_sub,
+                  void* beta, void* stream);
+
+/* Fused forward pass (Algorithm 1 = assemble + Decompose + Substitute,
+ * PAPER.md:216-234, 239-263, 293-315): y = M^{-1} beta per instance, with M
+ * and beta assembled in registers (never written to HBM) and the block
+ * Cholesky / substitution split over time chunks (DESIGN.md "Time-parallel
+ * partition solver").  `workspace` must hold smnn_workspace_bytes(p). */
+int smnn_factor_solve_fwd(const smnn_problem* p, const void* coeffs, const void* rhs,
+                          const void* iv, const void* steps, void* y, int32_t* info,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* Fused backward pass (Algorithm 2, chained
+ * through Appendix A.1): given y from the forward pass and grad_y = dl/dy,
+ * computes dl/dbeta = M^{-1} dl/dy by re-factoring M in registers, then
+ * dl/dcoeffs, dl/drhs, dl/div, dl/dsteps.  Any grad_* output may be NULL to
+ * skip it. */
+int smnn_solve_bwd(const smnn_problem* p, const void* coeffs, const void* rhs,
+                   const void* iv, const void* steps, const void* y, const void* grad_y,
+                   void* grad_coeffs, void* grad_rhs, void* grad_iv, void* grad_steps,
+                   int32_t* info, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Algorithm 3 "Decompose", materialised: one sequential
+ * sweep per instance writing L [n,T,b,b] and P [n,T-1,b,b] to HBM (the
+ * paper's own data flow; used for parity and as the sequential baseline).
+ * P may be NULL when T == 1. */
+int smnn_factor(const smnn_problem* p, const void* coeffs, const void* steps,
+                void* L, void* P, int32_t* info, void* stream);
+
+/* Algorithm 4 "Substitute": out = M^{-1} alpha from the
+ * materialised L, P of smnn_factor.  alpha, out: [n_inst, T, b]; may alias. */
+int smnn_substitute(const smnn_problem* p, const void* L, const void* P,
+                    const void* alpha, void* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Host-buffer end-to-end plan (the call a user makes with data in host RAM).
+ * A plan owns device buffers for one batch of shape `p`.  fwd_bwd_host copies
+ * the HOST inputs in, runs smnn_factor_solve_fwd then smnn_solve_bwd, and
+ * copies y and all gradients back to HOST memory, all on `stream`; it
+ * returns after the stream work is enqueued (synchronise the stream before
+ * reading the outputs).  Host buffers should be page-locked for overlap.
+ * ---------------------------------------------------------------------- */
+typedef struct smnn_plan smnn_plan;
+
+int smnn_plan_create(smnn_plan** plan, const smnn_problem* p);
+int smnn_plan_destroy(smnn_plan* plan);
+int smnn_plan_fwd_bwd_host(smnn_plan* plan, const void* coeffs, const void* rhs,
+                           const void* iv, const void* steps, const void* grad_y,
+                           void* y, void* grad_coeffs, void* grad_rhs, void* grad_iv,
+                           void* grad_steps, int32_t* info, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMNN_H_ */

@@ -1,0 +1,55 @@
+"""CPU checks of the C ABI boundary: the library builds/loads and exports every
+symbol include/smnn.h declares; argument validation runs without a GPU."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "smnn.h")).read()
+    return sorted(set(re.findall(r"\b(smnn_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2410_06074_b200 import _abi, build
+    build.build_library()
+    return _abi.load()
+
+
+def test_header_symbols_exported(lib):
+    from paper_2410_06074_b200 import _abi
+    syms = header_symbols()
+    assert set(syms) == set(_abi.EXPORTED), syms
+    for s in syms:
+        assert hasattr(lib, s), s
+
+
+def test_version_and_validation_without_gpu(lib):
+    from paper_2410_06074_b200 import _abi
+    assert b"sm_100a" in lib.smnn_version()
+    p = _abi.smnn_problem(n_inst=4, T=10, order=4, n_iv=1, dtype=0, threads_per_inst=0, reserved=0,
+                          w_gov=1, w_init=1, w_smooth=1)
+    rc = lib.smnn_factor_solve_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None)
+    assert rc == -3 and b"order" in lib.smnn_last_error()
+    p.order = 2
+    p.n_iv = 5
+    assert lib.smnn_assemble(ctypes.byref(p), None, None, None, None, None, None, None, None) == -1
+    p.n_iv = 2
+    p.w_smooth = 0.0
+    assert lib.smnn_factor(ctypes.byref(p), None, None, None, None, None, None) == -1
+    assert b"weights" in lib.smnn_last_error() or b"NULL" in lib.smnn_last_error()
+
+
+def test_product_path_refuses_cpu_tensors():
+    import torch
+    import paper_2410_06074_b200 as m
+    x = torch.zeros(2, 5, 3, dtype=torch.float64)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        m.smnn_factor_solve_fwd(x, torch.zeros(2, 5, dtype=torch.float64), torch.zeros(2, 2, dtype=torch.float64),
+                                torch.ones(2, 4, dtype=torch.float64))
