@@ -13,7 +13,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libsmnn.so")
 SOURCES = ["smnn_kernels.cu"]
-HEADERS = ["smnn_device.cuh", os.path.join(ROOT, "include", "smnn.h")]
+HEADERS = ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", os.path.join(ROOT, "include", "smnn.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -201,17 +201,4 @@ __device__ __forceinline__ void matmul(const T (&A)[B][B], const T (&Bm)[B][B], 
     }
 }
 
-template <int B, class T>
-__device__ __forceinline__ void zero(T (&A)[B][B]) {
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int j = 0; j < B; ++j) A[i][j] = T(0);
-}
-template <int B, class T>
-__device__ __forceinline__ void zero(T (&a)[B]) {
-#pragma unroll
-  for (int i = 0; i < B; ++i) a[i] = T(0);
-}
-
 }  // namespace smnn

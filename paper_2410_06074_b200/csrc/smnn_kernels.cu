@@ -27,57 +27,39 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "smnn.h"
 #include "smnn_device.cuh"
+#include "smnn_fused.cuh"
 
-#ifndef SMNN_MAX_THREADS
-#define SMNN_MAX_THREADS 256
+#ifndef SMNN_F32_LANE
+#define SMNN_F32_LANE float
+#endif
+#ifndef SMNN_F64_LANE
+#define SMNN_F64_LANE double
 #endif
 
 namespace smnn {
 
 // Register-segment length of pass 2 (steps whose factors stay in registers).
-template <int B, class Tc>
+template <int B, class S>
 struct SegLen {
-  static constexpr int value = (sizeof(Tc) == 8) ? (B <= 2 ? 8 : 4) : (B <= 3 ? 8 : 4);
+  static constexpr int value = (sizeof(S) >= 8) ? (B == 1 ? 8 : B == 2 ? 4 : 2) : (B <= 2 ? 8 : B == 3 ? 4 : 2);
 };
 
-// ------------------------------------------------------------------ args ----
-template <class Tio>
-struct Args {
-  const Tio* coeffs;
-  const Tio* rhs;
-  const Tio* iv;
-  const Tio* steps;
-  const Tio* y_in;     // BWD: forward solution
-  const Tio* grad_y;   // BWD: dl/dy
-  Tio* y_out;          // FWD: solution
-  Tio* g_coeffs;       // BWD outputs (nullable)
-  Tio* g_rhs;
-  Tio* g_iv;
-  Tio* g_steps;
-  int32_t* info;       // nullable
-  void* ckpt;          // workspace (Tc elements), one slot per block
-  int64_t n_inst;
-  int T;
-  int n_iv;
-  int K;               // chunks per instance (<= blockDim.x)
-  int nseg_ck;         // checkpoint segments per chunk (slot stride)
-  double wg2, wi2, ws2;
-};
+// Lane type of the fused kernels for (storage, arithmetic).
+template <class Tio, class Tc> struct LaneOf;
+template <> struct LaneOf<float, float> { using S = SMNN_F32_LANE; };
+template <> struct LaneOf<double, double> { using S = SMNN_F64_LANE; };
+template <> struct LaneOf<float, double> { using S = SMNN_F64_LANE; };
 
-template <int B>
-struct Ck {  // checkpoint element counts
-  static constexpr int L = B * B;  // Lf stored densely (simple indexing)
-  static constexpr int W = B;
-  static constexpr int X = B * B;
-  static constexpr int N = L + W + X;
-};
-
-// Load helpers ---------------------------------------------------------------
+// Load helpers (sequential kernels) ---------------------------------------
 template <int B, class Tio, class Tc>
 __device__ __forceinline__ void ld_vec(const Tio* p, Tc (&v)[B]) {
 #pragma unroll
@@ -86,10 +68,6 @@ __device__ __forceinline__ void ld_vec(const Tio* p, Tc (&v)[B]) {
 
 template <class Tio, class Tc>
 __device__ __forceinline__ Tc ld1(const Tio* p) { return Tc(__ldg(p)); }
-
-__device__ __forceinline__ int chunk_begin(int k, int T, int K) {
-  return int((int64_t(k) * T) / K);
-}
 
 // Per-instance base pointers (all further indexing is 32-bit).
 template <class Tio>
@@ -148,562 +126,6 @@ __device__ __forceinline__ void load_M(const View<Tio>& v, const W3& w, int j, c
 #pragma unroll
     for (int i = 0; i < B; ++i)
       if (i < v.n_iv) M[i][i] += Tc(w.i);
-  }
-}
-
-// dl/ds_j contribution of interval (j, j+1), PAPER.md:618-634 differentiated:
-//   -ws2 [ lj^T J+ yj + ln^T J- yn + ln^T K yj + yn^T K lj ]
-template <int B, class Tc>
-__device__ __forceinline__ Tc ds_interval(Tc s, Tc ws2, const Tc (&lj)[B], const Tc (&yj)[B], const Tc (&ln)[B],
-                                          const Tc (&yn)[B]) {
-  Tc q[2 * B - 1];  // q[m] = d/ds s^m = m s^{m-1}
-  Tc p[2 * B - 1];
-  powers<B, Tc>(s, p);
-  q[0] = Tc(0);
-#pragma unroll
-  for (int m = 1; m < 2 * B - 1; ++m) q[m] = Tc(m) * p[m - 1];
-  Tc acc = Tc(0);
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      const Tc g = Tc(Gc(i, k)) * q[i + k];
-      const Tc jp = g + (i == k ? q[2 * i] : Tc(0));
-      const Tc jm = Tc(sgn(i + k)) * g + (i == k ? q[2 * i] : Tc(0));
-      const Tc kd = -Tc(Hc(i, k)) * q[i + k];
-      acc += lj[i] * jp * yj[k] + ln[i] * (jm * yn[k] + kd * yj[k]) + yn[i] * kd * lj[k];
-    }
-  return -ws2 * acc;
-}
-
-// Gradients at point j (PAPER.md:626-634 differentiated, Eq. 13):
-//   dd_j = wg2 c.l ;  dc_j = wg2 ( d_j l - l (y.c) - y (l.c) ) ;  du = wi2 l_0.
-template <int B, class Tio, class Tc>
-__device__ __forceinline__ void point_grads(const View<Tio>& v, const W3& w, int j, const Tc (&lam)[B],
-                                            const Tc (&yj)[B]) {
-  Tc c[B];
-  ld_vec<B, Tio, Tc>(v.c + j * B, c);
-  Tc lc = Tc(0), yc = Tc(0);
-#pragma unroll
-  for (int i = 0; i < B; ++i) {
-    lc += lam[i] * c[i];
-    yc += yj[i] * c[i];
-  }
-  const Tc wg2 = Tc(w.g);
-  if (v.gd) v.gd[j] = Tio(wg2 * lc);
-  if (v.gc) {
-    const Tc d = ld1<Tio, Tc>(v.d + j);
-#pragma unroll
-    for (int i = 0; i < B; ++i) v.gc[j * B + i] = Tio(wg2 * (d * lam[i] - lam[i] * yc - yj[i] * lc));
-  }
-  if (j == 0 && v.gu) {
-    for (int i = 0; i < v.n_iv; ++i) v.gu[i] = Tio(Tc(w.i) * lam[i]);
-  }
-}
-
-// Shared-memory separator system, structure of arrays over the K separators.
-template <int B, class Tc>
-struct Sep {
-  Tc* D;   // [B*B][K]  diagonal block; holds the factor after elimination
-  Tc* Bc;  // [B*B][K]  coupling block(i, i-h); holds Y1 after elimination
-  Tc* Y2;  // [B*B][K]
-  Tc* R;   // [B][K]    rhs; holds v after elimination
-  Tc* Y;   // [B][K]    solution
-  int* time;  // [K]     time index of separator i (for info)
-  int* fail;  // [1]
-  int K;
-  __device__ void ld(const Tc* arr, int i, Tc (&m)[B][B]) const {
-#pragma unroll
-    for (int r = 0; r < B; ++r)
-#pragma unroll
-      for (int c = 0; c < B; ++c) m[r][c] = arr[(r * B + c) * K + i];
-  }
-  __device__ void st(Tc* arr, int i, const Tc (&m)[B][B]) const {
-#pragma unroll
-    for (int r = 0; r < B; ++r)
-#pragma unroll
-      for (int c = 0; c < B; ++c) arr[(r * B + c) * K + i] = m[r][c];
-  }
-  __device__ void ldv(const Tc* arr, int i, Tc (&v)[B]) const {
-#pragma unroll
-    for (int r = 0; r < B; ++r) v[r] = arr[r * K + i];
-  }
-  __device__ void stv(Tc* arr, int i, const Tc (&v)[B]) const {
-#pragma unroll
-    for (int r = 0; r < B; ++r) arr[r * K + i] = v[r];
-  }
-};
-
-// Block cyclic reduction of the separator system (SPD block tridiagonal).
-// All threads of the block must call it.
-template <int B, class Tc>
-__device__ __noinline__ void bcr_solve(Sep<B, Tc> S, int k) {
-  const int K = S.K;
-  int hmax = 0;
-#pragma unroll 1
-  for (int h = 1; h < K; h <<= 1) {
-    hmax = h;
-    if (k < K && (k % (2 * h)) == h) {
-      Tc D[B][B], Lf[B][B], Bk[B][B], Y1[B][B], Y2[B][B], r[B], v[B];
-      S.ld(S.D, k, D);
-      if (!chol<B, Tc>(D, Lf)) atomicMin(S.fail, S.time[k] + 1);
-      S.ld(S.Bc, k, Bk);
-      left_lsolve<B, Tc>(Lf, Bk, Y1);
-      if (k + h < K) {
-        Tc Bn[B][B], BnT[B][B];
-        S.ld(S.Bc, k + h, Bn);
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int j = 0; j < B; ++j) BnT[i][j] = Bn[j][i];
-        left_lsolve<B, Tc>(Lf, BnT, Y2);
-      } else {
-        zero<B, Tc>(Y2);
-      }
-      S.ldv(S.R, k, r);
-      lsolve<B, Tc>(Lf, r, v);
-      S.st(S.D, k, Lf);
-      S.st(S.Bc, k, Y1);
-      S.st(S.Y2, k, Y2);
-      S.stv(S.R, k, v);
-    }
-    __syncthreads();
-    if (k < K && (k % (2 * h)) == 0) {
-      Tc D[B][B], r[B];
-      S.ld(S.D, k, D);
-      S.ldv(S.R, k, r);
-      if (k - h >= 0) {
-        const int o = k - h;
-        Tc Y2o[B][B], Y1o[B][B], vo[B], nb[B][B];
-        S.ld(S.Y2, o, Y2o);
-        S.ld(S.Bc, o, Y1o);
-        S.ldv(S.R, o, vo);
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int j = 0; j < B; ++j) {
-            Tc accD = Tc(0), accB = Tc(0);
-#pragma unroll
-            for (int m = 0; m < B; ++m) {
-              accD += Y2o[m][i] * Y2o[m][j];
-              accB += Y2o[m][i] * Y1o[m][j];
-            }
-            D[i][j] -= accD;
-            nb[i][j] = (k - 2 * h >= 0) ? -accB : Tc(0);
-          }
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-          Tc acc = Tc(0);
-#pragma unroll
-          for (int m = 0; m < B; ++m) acc += Y2o[m][i] * vo[m];
-          r[i] -= acc;
-        }
-        S.st(S.Bc, k, nb);
-      }
-      if (k + h < K) {
-        const int o = k + h;
-        Tc Y1o[B][B], vo[B];
-        S.ld(S.Bc, o, Y1o);
-        S.ldv(S.R, o, vo);
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-#pragma unroll
-          for (int j = 0; j < B; ++j) {
-            Tc acc = Tc(0);
-#pragma unroll
-            for (int m = 0; m < B; ++m) acc += Y1o[m][i] * Y1o[m][j];
-            D[i][j] -= acc;
-          }
-          Tc acc = Tc(0);
-#pragma unroll
-          for (int m = 0; m < B; ++m) acc += Y1o[m][i] * vo[m];
-          r[i] -= acc;
-        }
-      }
-      S.st(S.D, k, D);
-      S.stv(S.R, k, r);
-    }
-    __syncthreads();
-  }
-  if (k == 0) {
-    Tc D[B][B], Lf[B][B], r[B], t[B], y[B];
-    S.ld(S.D, 0, D);
-    if (!chol<B, Tc>(D, Lf)) atomicMin(S.fail, S.time[0] + 1);
-    S.ldv(S.R, 0, r);
-    lsolve<B, Tc>(Lf, r, t);
-    ltsolve<B, Tc>(Lf, t, y);
-    S.stv(S.Y, 0, y);
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int h = hmax; h >= 1; h >>= 1) {
-    if (k < K && (k % (2 * h)) == h) {
-      Tc Lf[B][B], Y1[B][B], v[B], yl[B], t[B], y[B];
-      S.ld(S.D, k, Lf);
-      S.ld(S.Bc, k, Y1);
-      S.ldv(S.R, k, v);
-      S.ldv(S.Y, k - h, yl);
-      sub_matvec<B, Tc>(v, Y1, yl, t);
-      if (k + h < K) {
-        Tc Y2[B][B], yr[B], t2[B];
-        S.ld(S.Y2, k, Y2);
-        S.ldv(S.Y, k + h, yr);
-        sub_matvec<B, Tc>(t, Y2, yr, t2);
-#pragma unroll
-        for (int i = 0; i < B; ++i) t[i] = t2[i];
-      }
-      ltsolve<B, Tc>(Lf, t, y);
-      S.stv(S.Y, k, y);
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------- pass 1 ----
-// Factor the interior [f, l] of chunk k (l = sigma - 1), carry the spike and
-// write the Schur complement onto (sigma_{k-1}, sigma) plus the separator's
-// own block into shared memory (D, R, Bc) and the left-neighbour terms into
-// the temporaries (Y2 = A_ll, Y = r_l).
-template <int B, class Tio, class Tc, bool BWD, int G>
-__device__ __noinline__ void pass1(const View<Tio> v, const W3 w, Sep<B, Tc> S, Tc* ck, int k, int f, int sig) {
-  const int T = v.T;
-  const int K = S.K;
-  const int l = sig - 1;
-  const Tc ws2 = Tc(w.s);
-  Tc Arr[B][B], Arl[B][B], All[B][B], rr[B], rl[B];
-  zero<B, Tc>(Arr); zero<B, Tc>(Arl); zero<B, Tc>(All); zero<B, Tc>(rr); zero<B, Tc>(rl);
-  Tc pprev[2 * B - 1];
-  if (f < sig) {
-    Tc Lf[B][B], wv[B], X[B][B];
-    zero<B, Tc>(X);
-    zero<B, Tc>(Lf);
-    zero<B, Tc>(wv);
-    powers<B, Tc>((f > 0) ? ld1<Tio, Tc>(v.s + f - 1) : Tc(0), pprev);
-    Tc hp = (f > 0) ? Tc(1) : Tc(0);
-#pragma unroll 1
-    for (int j = f; j <= l; ++j) {
-      Tc c[B], pn[2 * B - 1], M[B][B], rhs[B], D[B][B], P[B][B];
-      ld_vec<B, Tio, Tc>(v.c + j * B, c);
-      powers<B, Tc>(ld1<Tio, Tc>(v.s + j), pn);
-      load_M<B, Tio, Tc>(v, w, j, c, pprev, hp, pn, Tc(1), M);
-      load_rhs<B, Tio, Tc, BWD>(v, w, j, c, rhs);
-      if (j > f) {
-        Tc Np[B][B], t[B];
-        assemble_N<B, Tc>(Np, pprev, ws2);
-        right_ltsolve<B, Tc>(Np, Lf, P);
-        sub_ppt<B, Tc>(M, P, D);
-        sub_matvec<B, Tc>(rhs, P, wv, t);
-#pragma unroll
-        for (int i = 0; i < B; ++i) rhs[i] = t[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int q = 0; q < B; ++q) D[i][q] = M[i][q];
-      }
-      if (!chol<B, Tc>(D, Lf)) atomicMin(S.fail, j + 1);
-      lsolve<B, Tc>(Lf, rhs, wv);
-      if (k > 0) {
-        Tc Y[B][B];
-        if (j == f) {
-          assemble_N<B, Tc>(Y, pprev, ws2);  // N_L = N_{f-1}
-          left_lsolve<B, Tc>(Lf, Y, X);
-        } else {
-          matmul<B, Tc>(P, X, Y);
-          left_lsolve<B, Tc>(Lf, Y, X);
-#pragma unroll
-          for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int q = 0; q < B; ++q) X[i][q] = -X[i][q];
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-#pragma unroll
-          for (int q = 0; q <= i; ++q) {
-            Tc acc = Tc(0);
-#pragma unroll
-            for (int m = 0; m < B; ++m) acc += X[m][i] * X[m][q];
-            All[i][q] -= acc;
-          }
-          Tc acc = Tc(0);
-#pragma unroll
-          for (int m = 0; m < B; ++m) acc += X[m][i] * wv[m];
-          rl[i] -= acc;
-        }
-      }
-      // checkpoint at the end of every full G-step segment (pass-2 resume point)
-      const int done = j - f + 1;
-      if ((done % G) == 0 && j < l) {
-        Tc* cp = ck + (done / G - 1) * Ck<B>::N * K + k;
-        int e = 0;
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int q = 0; q < B; ++q) cp[(e++) * K] = Lf[i][q];
-#pragma unroll
-        for (int i = 0; i < B; ++i) cp[(e++) * K] = wv[i];
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int q = 0; q < B; ++q) cp[(e++) * K] = X[i][q];
-      }
-#pragma unroll
-      for (int m = 0; m < 2 * B - 1; ++m) pprev[m] = pn[m];
-      hp = Tc(1);
-    }
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-#pragma unroll
-      for (int q = i + 1; q < B; ++q) All[i][q] = All[q][i];
-    // Schur complement of the interior onto the separators.
-    Tc NR[B][B], Pl[B][B];
-    assemble_N<B, Tc>(NR, pprev, ws2);  // N_l
-    right_ltsolve<B, Tc>(NR, Lf, Pl);
-#pragma unroll
-    for (int i = 0; i < B; ++i) {
-#pragma unroll
-      for (int q = 0; q < B; ++q) {
-        Tc acc = Tc(0), acc2 = Tc(0);
-#pragma unroll
-        for (int m = 0; m < B; ++m) {
-          acc += Pl[i][m] * Pl[q][m];
-          acc2 += Pl[i][m] * X[m][q];
-        }
-        Arr[i][q] = -acc;
-        Arl[i][q] = -acc2;
-      }
-      Tc acc = Tc(0);
-#pragma unroll
-      for (int m = 0; m < B; ++m) acc += Pl[i][m] * wv[m];
-      rr[i] = -acc;
-    }
-  } else {
-    // chunk of one point: direct coupling sigma_{k-1} -> sigma_k
-    powers<B, Tc>((sig > 0) ? ld1<Tio, Tc>(v.s + sig - 1) : Tc(0), pprev);
-    if (k > 0) assemble_N<B, Tc>(Arl, pprev, ws2);
-  }
-  // separator's own block and rhs
-  Tc c[B], pn[2 * B - 1], M[B][B], rhs[B];
-  ld_vec<B, Tio, Tc>(v.c + sig * B, c);
-  const bool hn = sig < T - 1;
-  powers<B, Tc>(hn ? ld1<Tio, Tc>(v.s + sig) : Tc(0), pn);
-  load_M<B, Tio, Tc>(v, w, sig, c, pprev, sig > 0 ? Tc(1) : Tc(0), pn, hn ? Tc(1) : Tc(0), M);
-  load_rhs<B, Tio, Tc, BWD>(v, w, sig, c, rhs);
-#pragma unroll
-  for (int i = 0; i < B; ++i) {
-    rhs[i] += rr[i];
-#pragma unroll
-    for (int q = 0; q < B; ++q) M[i][q] += Arr[i][q];
-  }
-  S.st(S.D, k, M);
-  S.stv(S.R, k, rhs);
-  S.st(S.Bc, k, Arl);
-  S.st(S.Y2, k, All);  // temporaries, consumed by the left neighbour
-  S.stv(S.Y, k, rl);
-}
-
-// ---------------------------------------------------------------- pass 2 ----
-// Interior solve of chunk k with both separator values known, in G-step
-// register segments processed last-to-first; FWD writes y, BWD writes the
-// gradients (lam = dl/dbeta is the solution here, y comes from the forward).
-template <int B, class Tio, class Tc, bool BWD, int G>
-__device__ __noinline__ void pass2(const View<Tio> v, const W3 w, Sep<B, Tc> S, const Tc* ck, int k, int f,
-                                   int sig) {
-  const int K = S.K;
-  const int l = sig - 1;
-  const Tc ws2 = Tc(w.s);
-  Tc yR[B], yL[B], ysR[B];
-  S.ldv(S.Y, k, yR);
-  if (k > 0) S.ldv(S.Y, k - 1, yL); else zero<B, Tc>(yL);
-  zero<B, Tc>(ysR);
-  if (!BWD) {
-#pragma unroll
-    for (int i = 0; i < B; ++i) v.yout[sig * B + i] = Tio(yR[i]);
-  } else {
-    ld_vec<B, Tio, Tc>(v.yin + sig * B, ysR);
-    point_grads<B, Tio, Tc>(v, w, sig, yR, ysR);
-  }
-  Tc ynext[B], yfn[B];  // solution / forward y of the point after the current one
-#pragma unroll
-  for (int i = 0; i < B; ++i) { ynext[i] = yR[i]; yfn[i] = ysR[i]; }
-  if (f < sig) {
-    const int nint = l - f + 1;
-    const int nseg = (nint + G - 1) / G;
-#pragma unroll 1
-    for (int seg = nseg - 1; seg >= 0; --seg) {
-      const int j0 = f + seg * G;
-      const int len = min(G, l + 1 - j0);
-      Tc Lp[B][B], wp[B], pprev[2 * B - 1];
-      Tc hp;
-      if (seg > 0) {
-        const Tc* cp = ck + (seg - 1) * Ck<B>::N * K + k;
-        int e = 0;
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int q = 0; q < B; ++q) Lp[i][q] = cp[(e++) * K];
-#pragma unroll
-        for (int i = 0; i < B; ++i) wp[i] = cp[(e++) * K];
-        if (k > 0) {  // w' = w - X y_L  (left-separator correction)
-#pragma unroll
-          for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int q = 0; q < B; ++q) wp[i] -= cp[(B * B + B + i * B + q) * K] * yL[q];
-        }
-        powers<B, Tc>(ld1<Tio, Tc>(v.s + j0 - 1), pprev);
-        hp = Tc(1);
-      } else {
-        zero<B, Tc>(Lp);
-        zero<B, Tc>(wp);
-        powers<B, Tc>((f > 0) ? ld1<Tio, Tc>(v.s + f - 1) : Tc(0), pprev);
-        hp = (f > 0) ? Tc(1) : Tc(0);
-      }
-      Tc Lr[G][B][B], Wr[G][B];
-#pragma unroll
-      for (int i = 0; i < G; ++i) {
-        if (i < len) {
-          const int j = j0 + i;
-          Tc c[B], pn[2 * B - 1], M[B][B], rhs[B], D[B][B];
-          ld_vec<B, Tio, Tc>(v.c + j * B, c);
-          powers<B, Tc>(ld1<Tio, Tc>(v.s + j), pn);
-          load_M<B, Tio, Tc>(v, w, j, c, pprev, hp, pn, Tc(1), M);
-          load_rhs<B, Tio, Tc, BWD>(v, w, j, c, rhs);
-          if (j == f && k > 0) {  // left separator: rhs -= N_{f-1} y_L
-            Tc NL[B][B], t[B];
-            assemble_N<B, Tc>(NL, pprev, ws2);
-            sub_matvec<B, Tc>(rhs, NL, yL, t);
-#pragma unroll
-            for (int q = 0; q < B; ++q) rhs[q] = t[q];
-          }
-          if (j > f) {
-            Tc Np[B][B], P[B][B], t[B];
-            assemble_N<B, Tc>(Np, pprev, ws2);
-            right_ltsolve<B, Tc>(Np, Lp, P);
-            sub_ppt<B, Tc>(M, P, D);
-            sub_matvec<B, Tc>(rhs, P, wp, t);
-#pragma unroll
-            for (int q = 0; q < B; ++q) rhs[q] = t[q];
-          } else {
-#pragma unroll
-            for (int q = 0; q < B; ++q)
-#pragma unroll
-              for (int r = 0; r < B; ++r) D[q][r] = M[q][r];
-          }
-          if (j == l) {  // right separator: rhs -= N_l^T y_R
-            Tc NR[B][B], t[B];
-            assemble_N<B, Tc>(NR, pn, ws2);
-            matTvec<B, Tc>(NR, yR, t);
-#pragma unroll
-            for (int q = 0; q < B; ++q) rhs[q] -= t[q];
-          }
-          chol<B, Tc>(D, Lr[i]);
-          lsolve<B, Tc>(Lr[i], rhs, Wr[i]);
-#pragma unroll
-          for (int q = 0; q < B; ++q) {
-            wp[q] = Wr[i][q];
-#pragma unroll
-            for (int r = 0; r <= q; ++r) Lp[q][r] = Lr[i][q][r];
-          }
-#pragma unroll
-          for (int m = 0; m < 2 * B - 1; ++m) pprev[m] = pn[m];
-          hp = Tc(1);
-        }
-      }
-#pragma unroll
-      for (int i = G - 1; i >= 0; --i) {
-        if (i < len) {
-          const int j = j0 + i;
-          Tc yv[B];
-          const Tc sj = ld1<Tio, Tc>(v.s + j);
-          if (j == l) {
-            ltsolve<B, Tc>(Lr[i], Wr[i], yv);
-          } else {
-            Tc pw[2 * B - 1], Nj[B][B], vv[B], u[B], t[B];
-            powers<B, Tc>(sj, pw);
-            assemble_N<B, Tc>(Nj, pw, ws2);
-            matTvec<B, Tc>(Nj, ynext, vv);
-            lsolve<B, Tc>(Lr[i], vv, u);
-#pragma unroll
-            for (int q = 0; q < B; ++q) t[q] = Wr[i][q] - u[q];
-            ltsolve<B, Tc>(Lr[i], t, yv);
-          }
-          if (!BWD) {
-#pragma unroll
-            for (int q = 0; q < B; ++q) v.yout[j * B + q] = Tio(yv[q]);
-          } else {
-            Tc yf[B];
-            ld_vec<B, Tio, Tc>(v.yin + j * B, yf);
-            point_grads<B, Tio, Tc>(v, w, j, yv, yf);
-            if (v.gs) v.gs[j] = Tio(ds_interval<B, Tc>(sj, ws2, yv, yf, ynext, yfn));
-#pragma unroll
-            for (int q = 0; q < B; ++q) yfn[q] = yf[q];
-          }
-#pragma unroll
-          for (int q = 0; q < B; ++q) ynext[q] = yv[q];
-        }
-      }
-    }
-  }
-  // BWD: interval (sigma_{k-1}, first point of the chunk)
-  if (BWD && k > 0 && v.gs) {
-    const int jm = f - 1;
-    Tc yfm[B];
-    ld_vec<B, Tio, Tc>(v.yin + jm * B, yfm);
-    v.gs[jm] = Tio(ds_interval<B, Tc>(ld1<Tio, Tc>(v.s + jm), ws2, yL, yfm, ynext, yfn));
-  }
-}
-
-// ------------------------------------------------------ the fused kernel ----
-template <int B, class Tio, class Tc, bool BWD, int G>
-__global__ void __launch_bounds__(SMNN_MAX_THREADS) fused_kernel(Args<Tio> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = a.K;
-  Tc* base = reinterpret_cast<Tc*>(smem_raw);
-  Sep<B, Tc> S;
-  S.D = base;
-  S.Bc = S.D + B * B * K;
-  S.Y2 = S.Bc + B * B * K;
-  S.R = S.Y2 + B * B * K;
-  S.Y = S.R + B * K;
-  S.time = reinterpret_cast<int*>(S.Y + B * K);
-  S.fail = S.time + K;
-  S.K = K;
-  const W3 w{a.wg2, a.wi2, a.ws2};
-  const int k = threadIdx.x;
-  const int T = a.T;
-  Tc* ck = reinterpret_cast<Tc*>(a.ckpt) + size_t(blockIdx.x) * size_t(a.nseg_ck) * Ck<B>::N * K;
-
-  for (int64_t inst = blockIdx.x; inst < a.n_inst; inst += gridDim.x) {
-    if (k == 0) *S.fail = INT_MAX;
-    const View<Tio> v(a, inst, B);
-    const int f = (k < K) ? chunk_begin(k, T, K) : 0;
-    const int sig = (k < K) ? chunk_begin(k + 1, T, K) - 1 : 0;
-    if (k < K) {
-      S.time[k] = sig;
-      pass1<B, Tio, Tc, BWD, G>(v, w, S, ck, k, f, sig);
-    }
-    __syncthreads();
-    if (k + 1 < K) {  // add the right neighbour's Schur terms A_ll, r_l
-      Tc D[B][B], Al[B][B], r[B], rl[B];
-      S.ld(S.D, k, D);
-      S.ld(S.Y2, k + 1, Al);
-      S.ldv(S.R, k, r);
-      S.ldv(S.Y, k + 1, rl);
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-        r[i] += rl[i];
-#pragma unroll
-        for (int q = 0; q < B; ++q) D[i][q] += Al[i][q];
-      }
-      S.st(S.D, k, D);
-      S.stv(S.R, k, r);
-    }
-    __syncthreads();
-    bcr_solve<B, Tc>(S, k);
-    if (k < K) pass2<B, Tio, Tc, BWD, G>(v, w, S, ck, k, f, sig);
-    __syncthreads();
-    if (k == 0 && a.info) a.info[inst] = (*S.fail == INT_MAX) ? 0 : *S.fail;
-    __syncthreads();
   }
 }
 
@@ -876,33 +298,53 @@ int validate(const smnn_problem* p) {
 
 size_t tc_size(const smnn_problem* p) { return p->dtype == SMNN_F32 ? 4 : 8; }
 
+// Lane of the fused kernels: P instances per register, `bytes` per lane value.
+struct LaneInfo {
+  int P;
+  size_t bytes;
+};
+LaneInfo lane_info(const smnn_problem* p) {
+  if (p->dtype == SMNN_F32) return {smnn::LaneT<SMNN_F32_LANE>::P, sizeof(SMNN_F32_LANE)};
+  return {smnn::LaneT<SMNN_F64_LANE>::P, sizeof(SMNN_F64_LANE)};
+}
+
 int pass2_G(const smnn_problem* p) {
   const int B = p->order + 1;
-  if (tc_size(p) == 8) return B <= 2 ? 8 : 4;
-  return B <= 3 ? 8 : 4;  // == smnn::SegLen<B, Tc>::value
+  return lane_info(p).bytes >= 8 ? (B == 1 ? 8 : B == 2 ? 4 : 2) : (B <= 2 ? 8 : B == 3 ? 4 : 2);  // == SegLen
+}
+
+size_t sep_bytes_per_chunk(const smnn_problem* p) {
+  const int B = p->order + 1;
+  return size_t(3 * B * B + 2 * B) * lane_info(p).bytes + sizeof(int);
+}
+
+// Target steps per time chunk (env SMNN_CHUNK overrides, for tuning).
+int chunk_target() {
+  static int m = 0;
+  if (m == 0) {
+    const char* e = std::getenv("SMNN_CHUNK");
+    m = e ? std::max(2, std::atoi(e)) : 16;
+  }
+  return m;
 }
 
 // Chunks (threads) per instance.
 int threads_per_inst(const smnn_problem* p) {
   int nt = p->threads_per_inst;
   if (nt == 0) {
-    const int target = 16;  // interior steps per chunk
+    const int target = chunk_target();  // steps per chunk
     nt = (p->T + target - 1) / target;
     nt = ((nt + 31) / 32) * 32;
     nt = std::max(32, std::min(nt, SMNN_MAX_THREADS));
   }
-  const int B = p->order + 1;
-  const size_t per = size_t(3 * B * B + 2 * B) * tc_size(p) + 8;
-  while (nt > 32 && per * nt > 160 * 1024) nt -= 32;
+  while (nt > 32 && sep_bytes_per_chunk(p) * nt > 160 * 1024) nt -= 32;
   return nt;
 }
 
 int chunks(const smnn_problem* p) { return std::min(threads_per_inst(p), p->T); }
 
 size_t fused_smem(const smnn_problem* p) {
-  const int B = p->order + 1;
-  const int K = chunks(p);
-  return size_t(3 * B * B + 2 * B) * K * tc_size(p) + size_t(K + 1) * sizeof(int) + 16;
+  return sep_bytes_per_chunk(p) * chunks(p) + 4 * sizeof(int) + 16;
 }
 
 int nseg_ck(const smnn_problem* p) {
@@ -915,35 +357,54 @@ int nseg_ck(const smnn_problem* p) {
 
 size_t ck_elems(const smnn_problem* p) {
   const int B = p->order + 1;
-  return size_t(2 * B * B + B);
+  return size_t(B * (B + 1) / 2 + B + B * B);  // == smnn::CkN<B>::N
+}
+
+int64_t n_groups(const smnn_problem* p) {
+  const int P = lane_info(p).P;
+  return (p->n_inst + P - 1) / P;
 }
 
 int device_sms() {
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms = v;
+  }
   return sms;
 }
 
-// Persistent grid: resident blocks, capped by the number of instances.
-template <class K>
-int fused_grid(K kernel, const smnn_problem* p) {
+// Occupancy of a kernel (cached per kernel / block / smem).
+std::mutex g_occ_mu;
+std::map<std::tuple<const void*, int, size_t>, int> g_occ;
+
+template <class Kern>
+int occupancy(Kern kernel, int nt, size_t smem) {
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), nt, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+  }
   int occ = 1;
-  const int nt = threads_per_inst(p);
-  const size_t smem = fused_smem(p);
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, smem);
   occ = std::max(occ, 1);
-  const int64_t g = std::min<int64_t>(p->n_inst, int64_t(occ) * device_sms());
-  return int(std::max<int64_t>(g, 1));
+  std::lock_guard<std::mutex> lk(g_occ_mu);
+  g_occ[key] = occ;
+  return occ;
 }
 
 template <int B, class Tio, class Tc>
 int fused_grid_any(const smnn_problem* p) {
-  using namespace smnn;
-  constexpr int G = SegLen<B, Tc>::value;
-  const int g1 = fused_grid(fused_kernel<B, Tio, Tc, false, G>, p);
-  const int g2 = fused_grid(fused_kernel<B, Tio, Tc, true, G>, p);
-  return std::max(g1, g2);
+  using S = typename smnn::LaneOf<Tio, Tc>::S;
+  constexpr int G = smnn::SegLen<B, S>::value;
+  const int nt = threads_per_inst(p);
+  const size_t smem = fused_smem(p);
+  const int occ = std::max(occupancy(smnn::fused_kernel<B, Tio, S, false, G>, nt, smem),
+                           occupancy(smnn::fused_kernel<B, Tio, S, true, G>, nt, smem));
+  return int(std::max<int64_t>(1, std::min<int64_t>(n_groups(p), int64_t(occ) * device_sms())));
 }
 
 template <class Tio, class Tc>
@@ -963,7 +424,7 @@ int grid_blocks(const smnn_problem* p) {
 }
 
 size_t workspace_bytes(const smnn_problem* p) {
-  const size_t per = size_t(nseg_ck(p)) * ck_elems(p) * chunks(p) * tc_size(p);
+  const size_t per = size_t(nseg_ck(p)) * ck_elems(p) * chunks(p) * lane_info(p).bytes;
   return std::max<size_t>(per * grid_blocks(p), 256);
 }
 
@@ -982,13 +443,131 @@ smnn::Args<Tio> make_args(const smnn_problem* p) {
   return a;
 }
 
+// ---------------------------------------------------------------- resident --
+struct RPlan {
+  smnn::RLayout L;
+  size_t smem = 0;
+  bool ok = false;
+};
+
+size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Largest cluster the resident kernel may use (env SMNN_MAX_CLUSTER; default 1:
+// measured on B200, DSMEM cluster BCR is slower than the streaming kernel).
+int max_cluster() {
+  static int c = 0;
+  if (c == 0) {
+    const char* e = std::getenv("SMNN_MAX_CLUSTER");
+    c = e ? std::max(1, std::min(16, std::atoi(e))) : 1;
+  }
+  return c;
+}
+
+// Shared-memory layout of the resident kernel for (problem, direction): the
+// smallest cluster whose CTAs each hold their time range of the instance.
+template <int B, class Tio, class S>
+RPlan resident_plan(const smnn_problem* p, bool bwd) {
+  RPlan best;
+  const char* env = std::getenv("SMNN_KERNEL");
+  if (env && std::string(env) == "stream") return best;
+  const size_t es = sizeof(Tio), ls = sizeof(S);
+  constexpr int G = smnn::SegLen<B, S>::value;
+  const int T = p->T;
+  const size_t budgets[2] = {110 * 1024, 200 * 1024};
+  for (size_t budget : budgets) {
+    for (int cs = 1; cs <= max_cluster(); cs *= 2) {
+      int nt = p->threads_per_inst;
+      if (nt == 0) {
+        const int m = chunk_target();  // steps per chunk
+        nt = (T + cs * m - 1) / (cs * m);
+        nt = std::max(32, std::min(((nt + 31) / 32) * 32, SMNN_MAX_THREADS));
+      }
+      if (int64_t(cs) * nt > T) {
+        nt = (T / cs / 32) * 32;
+        if (nt < 32) break;
+      }
+      const int K = cs * nt;
+      const int maxchunk = (T + K - 1) / K;
+      const int Lmax = nt * maxchunk;
+      smnn::RLayout L{};
+      L.nt = nt;
+      L.cs = cs;
+      size_t off = 0;
+      auto take = [&](size_t bytes) { const size_t o = off; off = al16(off + bytes); return int(o); };
+      L.off_c = take(size_t(Lmax) * B * es + 32);
+      L.off_d = take(size_t(Lmax) * es + 32);
+      L.off_s = take(size_t(Lmax + 1) * es + 32);
+      L.off_g = bwd ? take(size_t(Lmax) * B * es + 32) : 0;
+      L.off_y = bwd ? take(size_t(Lmax + 1) * B * es + 32) : 0;
+      L.off_sep = take(size_t(3 * B * B + 2 * B) * nt * ls + size_t(nt + 4) * 4);
+      const int nck = std::max(0, (maxchunk - 1 + G - 1) / G - 1);
+      L.off_ck = take(size_t(nck) * smnn::CkN<B>::N * nt * ls + 16);
+      L.off_bar = take(16);
+      if (off <= budget) {
+        best.L = L;
+        best.smem = off;
+        best.ok = true;
+        return best;
+      }
+    }
+  }
+  return best;
+}
+
+template <int B, class Tio, class Tc, bool BWD>
+int launch_resident(const smnn_problem* p, const smnn::Args<Tio>& a, const RPlan& rp, cudaStream_t st) {
+  using S = typename smnn::LaneOf<Tio, Tc>::S;
+  auto kern = rp.L.cs > 1 ? smnn::resident_kernel<B, Tio, S, BWD, smnn::SegLen<B, S>::value, true>
+                          : smnn::resident_kernel<B, Tio, S, BWD, smnn::SegLen<B, S>::value, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rp.smem));
+  if (rp.L.cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = rp.L.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(rp.L.nt);
+  cfg.dynamicSmemBytes = rp.smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(rp.L.cs);
+  int nclusters = 0;
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), rp.L.cs, rp.L.nt, rp.smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) nclusters = it->second;
+  }
+  if (nclusters == 0) {
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      nclusters = std::max(1, device_sms() / rp.L.cs);
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = nclusters;
+  }
+  const int64_t nc = std::min<int64_t>(p->n_inst, nclusters);
+  cfg.gridDim = dim3(unsigned(nc * rp.L.cs));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, rp.L);
+  return check_cuda(e == cudaSuccess ? cudaGetLastError() : e, "resident kernel launch");
+}
+
 template <int B, class Tio, class Tc, bool BWD>
 int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
+  using S = typename smnn::LaneOf<Tio, Tc>::S;
+  if (smnn::LaneT<S>::P == 1) {
+    const RPlan rp = resident_plan<B, Tio, S>(p, BWD);
+    if (rp.ok) return launch_resident<B, Tio, Tc, BWD>(p, a, rp, st);
+  }
   const int nt = threads_per_inst(p);
   const size_t smem = fused_smem(p);
   const int grid = grid_blocks(p);
-  auto k = smnn::fused_kernel<B, Tio, Tc, BWD, smnn::SegLen<B, Tc>::value>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  auto k = smnn::fused_kernel<B, Tio, S, BWD, smnn::SegLen<B, S>::value>;
+  occupancy(k, nt, smem);  // sets the dynamic smem attribute once
   k<<<grid, nt, smem, st>>>(a);
   return check_cuda(cudaGetLastError(), "fused kernel launch");
 }
