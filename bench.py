@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="lorenz", choices=sorted(WORKLOADS))
-    ap.add_argument("--dtype", default="f32", choices=["f32", "f64", "f32c64"])
+    ap.add_argument("--dtype", default=None, choices=["f32", "f64", "f32c64"],
+                    help="default: f32, except order-3 workloads (kdv): f32c64, because fp32 "
+                         "normal equations break down there (DESIGN.md 'Conditioning')")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threads-per-inst", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -180,6 +182,8 @@ def run_reference(args, wl):
 def main():
     args = parse()
     wl = WORKLOADS[args.workload]
+    if args.dtype is None:
+        args.dtype = "f32c64" if wl.order >= 3 else "f32"
     if args.impl == "reference":
         run_reference(args, wl)
         return
@@ -258,6 +262,10 @@ def main():
     kbytes = inst_steps * (bb if b_avg >= f_avg else fb)
     kms = max(b_avg, f_avg)
     achieved = kbytes / (kms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):  # measured by ncu on the GPU box (see profiles/README.md)
+        traffic = json.load(open(tp)).get(f"{wl.name}/{args.dtype}/{kern}")
     step_gbs = inst_steps * (fb + bb) / (ms_per_step / 1e3) / 1e9
 
     # end-to-end through the host-buffer C-ABI plan (H2D + fwd + bwd + D2H)
@@ -307,7 +315,7 @@ def main():
                        "parallelism": f"dp{world} (instances sharded, no data-path collective)",
                        "threads_per_inst": tpi or "auto"},
             "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": kbytes, "launch_ms": kms,
                          "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
             "kernels_ms": {"smnn_factor_solve_fwd": f_avg, "smnn_solve_bwd": b_avg},

@@ -51,7 +51,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
             _build.build_library()
         else:
             raise RuntimeError(f"{_build.LIB} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
-    L = ctypes.CDLL(_build.LIB)
+    path = os.environ.get("SMNN_LIB", _build.LIB)  # alternative builds, for experiments
+    L = ctypes.CDLL(path)
     L.smnn_version.restype = ctypes.c_char_p
     L.smnn_version.argtypes = []
     L.smnn_last_error.restype = ctypes.c_char_p

@@ -30,6 +30,11 @@
 #ifndef SMNN_MIN_BLOCKS
 #define SMNN_MIN_BLOCKS 2
 #endif
+// Warp-tiled two-ended separator reduction (measured slower than the packed
+// CTA-wide BCR on B200 for K <= 256; kept for experiments).
+#ifndef SMNN_WARP_BCR
+#define SMNN_WARP_BCR 0
+#endif
 
 namespace smnn {
 
@@ -441,10 +446,252 @@ __device__ __noinline__ void lbcr(SepL<B, S, CL> Sp, int k) {
   }
 }
 
+// Warp-tiled two-ended block cyclic reduction (one CTA).  Separator i sits in
+// warp w = i / 32 at slot q = i % 32 + 1; slot q = 0 is the warp's virtual
+// left port (separator 32w - 1, owned by warp w - 1), whose diagonal / rhs
+// contributions accumulate in PW.  Each warp eliminates its slots 1..31 by
+// odd-even reduction (5 levels, __syncwarp only), keeping both ends; one thread
+// then solves the W-block system of the ports (slot 32 of every warp); each
+// warp back-substitutes its own slots.  Two __syncthreads in total.
+// Separator slots >= K must hold identity blocks (dummies).
+template <class S, int B>
+struct PortW {  // per-warp scratch (W <= 32 warps), AoS
+  S* D0;  // [W][B*B]  left-port diagonal contributions
+  S* R0;  // [W][B]
+  S* Y0;  // [W][B]    left-port solution
+  S* TL;  // [W][B*B]  top-level factor
+  S* TP;  // [W][B*B]
+  S* TZ;  // [W][B]
+};
+
+template <int B, class S, int P>
+__device__ __noinline__ void lbcr_warp(SepL<B, S, false> Sp, PortW<S, B> PW, int k, int nt) {
+  const int w = k >> 5, lane = k & 31, W = nt >> 5;
+  const int base = w * 32 - 1;  // separator index of slot q is base + q
+  auto ldD = [&](int q, S (&m)[B][B]) {
+    if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < B * B; ++i) m[i / B][i % B] = PW.D0[w * B * B + i];
+    } else {
+      Sp.ld(Sp.D, base + q, m);
+    }
+  };
+  auto stD = [&](int q, const S (&m)[B][B]) {
+    if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < B * B; ++i) PW.D0[w * B * B + i] = m[i / B][i % B];
+    } else {
+      Sp.st(Sp.D, base + q, m);
+    }
+  };
+  auto ldR = [&](int q, S (&v)[B]) {
+    if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < B; ++i) v[i] = PW.R0[w * B + i];
+    } else {
+      Sp.ldv(Sp.R, base + q, v);
+    }
+  };
+  auto stR = [&](int q, const S (&v)[B]) {
+    if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < B; ++i) PW.R0[w * B + i] = v[i];
+    } else {
+      Sp.stv(Sp.R, base + q, v);
+    }
+  };
+  if (lane == 0) {  // the left port starts with no contributions
+#pragma unroll
+    for (int i = 0; i < B * B; ++i) PW.D0[w * B * B + i] = splat<S>(0.0);
+#pragma unroll
+    for (int i = 0; i < B; ++i) PW.R0[w * B + i] = splat<S>(0.0);
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int h = 1; h <= 16; h <<= 1) {
+    const int o = h * (2 * lane + 1);
+    if (o < 32) {  // eliminate slot o (neighbours o - h >= 0, o + h <= 32)
+      S D[B][B], Lf[B][B], Bk[B][B], Bn[B][B], BnT[B][B], Y1[B][B], Y2[B][B], r[B], v[B];
+      Sp.ld(Sp.D, base + o, D);
+      report<P>(Sp.fail, lchol<B, S>(D, Lf), Sp.ltime(base + o));
+      Sp.ld(Sp.Bc, base + o, Bk);
+      lleft<B, S>(Lf, Bk, Y1);
+      Sp.ld(Sp.Bc, base + o + h, Bn);
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int j = 0; j < B; ++j) BnT[i][j] = Bn[j][i];
+      lleft<B, S>(Lf, BnT, Y2);
+      Sp.ldv(Sp.R, base + o, r);
+      llsolve<B, S>(Lf, r, v);
+      Sp.st(Sp.D, base + o, Lf);
+      Sp.st(Sp.Bc, base + o, Y1);
+      Sp.st(Sp.Y2, base + o, Y2);
+      Sp.stv(Sp.R, base + o, v);
+    }
+    __syncwarp();
+    const int e = 2 * h * lane;
+    if (e <= 32) {  // update survivor e from its eliminated neighbours
+      S D[B][B], r[B];
+      ldD(e, D);
+      ldR(e, r);
+      if (e >= h) {
+        const int oo = e - h;
+        S Y2o[B][B], Y1o[B][B], vo[B], nb[B][B];
+        Sp.ld(Sp.Y2, base + oo, Y2o);
+        Sp.ld(Sp.Bc, base + oo, Y1o);
+        Sp.ldv(Sp.R, base + oo, vo);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            S aD = D[i][j], aB = splat<S>(0.0);
+#pragma unroll
+            for (int m = 0; m < B; ++m) {
+              aD = fnma_(Y2o[m][i], Y2o[m][j], aD);
+              aB = fnma_(Y2o[m][i], Y1o[m][j], aB);
+            }
+            D[i][j] = aD;
+            nb[i][j] = (e - 2 * h >= 0) ? aB : splat<S>(0.0);
+          }
+          S ar = r[i];
+#pragma unroll
+          for (int m = 0; m < B; ++m) ar = fnma_(Y2o[m][i], vo[m], ar);
+          r[i] = ar;
+        }
+        Sp.st(Sp.Bc, base + e, nb);
+      }
+      if (e + h <= 32) {
+        const int oo = e + h;
+        S Y1o[B][B], vo[B];
+        Sp.ld(Sp.Bc, base + oo, Y1o);
+        Sp.ldv(Sp.R, base + oo, vo);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            S aD = D[i][j];
+#pragma unroll
+            for (int m = 0; m < B; ++m) aD = fnma_(Y1o[m][i], Y1o[m][j], aD);
+            D[i][j] = aD;
+          }
+          S ar = r[i];
+#pragma unroll
+          for (int m = 0; m < B; ++m) ar = fnma_(Y1o[m][i], vo[m], ar);
+          r[i] = ar;
+        }
+      }
+      stD(e, D);
+      stR(e, r);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (k == 0) {  // block-tridiagonal Cholesky of the W ports (slot 32 of each warp)
+    S Lp[B][B], zp[B];
+    zero<B, S>(Lp);
+    zero<B, S>(zp);
+    for (int v = 0; v < W; ++v) {
+      const int iv = 32 * v + 31;
+      S D[B][B], r[B], Lf[B][B], z[B];
+      Sp.ld(Sp.D, iv, D);
+      Sp.ldv(Sp.R, iv, r);
+      if (v + 1 < W) {
+#pragma unroll
+        for (int i = 0; i < B * B; ++i) D[i / B][i % B] = add_(D[i / B][i % B], PW.D0[(v + 1) * B * B + i]);
+#pragma unroll
+        for (int i = 0; i < B; ++i) r[i] = add_(r[i], PW.R0[(v + 1) * B + i]);
+      }
+      if (v > 0) {
+        S C[B][B], Pm[B][B];
+        Sp.ld(Sp.Bc, iv, C);  // block(port v, port v-1)
+#pragma unroll
+        for (int rr = 0; rr < B; ++rr) llsolve<B, S>(Lp, C[rr], Pm[rr]);
+        lcouple<B, S>(Pm, zp, D, r);
+#pragma unroll
+        for (int i = 0; i < B * B; ++i) PW.TP[v * B * B + i] = Pm[i / B][i % B];
+      }
+      report<P>(Sp.fail, lchol<B, S>(D, Lf), Sp.ltime(iv));
+      llsolve<B, S>(Lf, r, z);
+#pragma unroll
+      for (int i = 0; i < B * B; ++i) PW.TL[v * B * B + i] = Lf[i / B][i % B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) PW.TZ[v * B + i] = z[i];
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        zp[i] = z[i];
+#pragma unroll
+        for (int j = 0; j < B; ++j) Lp[i][j] = Lf[i][j];
+      }
+    }
+    S yn[B];
+    zero<B, S>(yn);
+    for (int v = W - 1; v >= 0; --v) {
+      S Lf[B][B], z[B], y[B];
+#pragma unroll
+      for (int i = 0; i < B * B; ++i) Lf[i / B][i % B] = PW.TL[v * B * B + i];
+#pragma unroll
+      for (int i = 0; i < B; ++i) z[i] = PW.TZ[v * B + i];
+      if (v + 1 < W) {  // z -= P_{v+1}^T y_{v+1}
+        S Pn[B][B];
+#pragma unroll
+        for (int i = 0; i < B * B; ++i) Pn[i / B][i % B] = PW.TP[(v + 1) * B * B + i];
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int m = 0; m < B; ++m) z[i] = fnma_(Pn[m][i], yn[m], z[i]);
+      }
+      lltsolve<B, S>(Lf, z, y);
+      Sp.stv(Sp.Y, 32 * v + 31, y);
+      if (v + 1 < W) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) PW.Y0[(v + 1) * B + i] = y[i];
+      }
+#pragma unroll
+      for (int i = 0; i < B; ++i) yn[i] = y[i];
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) PW.Y0[i] = splat<S>(0.0);  // warp 0 has no left port
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int h = 16; h >= 1; h >>= 1) {
+    const int o = h * (2 * lane + 1);
+    if (o < 32) {
+      S Lf[B][B], Y1[B][B], Y2[B][B], v[B], yl[B], yr[B], t[B], y[B];
+      Sp.ld(Sp.D, base + o, Lf);
+      Sp.ld(Sp.Bc, base + o, Y1);
+      Sp.ld(Sp.Y2, base + o, Y2);
+      Sp.ldv(Sp.R, base + o, v);
+      if (o - h == 0) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) yl[i] = PW.Y0[w * B + i];
+      } else {
+        Sp.ldv(Sp.Y, base + o - h, yl);
+      }
+      Sp.ldv(Sp.Y, base + o + h, yr);
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        S acc = v[i];
+#pragma unroll
+        for (int m = 0; m < B; ++m) acc = fnma_(Y2[i][m], yr[m], fnma_(Y1[i][m], yl[m], acc));
+        t[i] = acc;
+      }
+      lltsolve<B, S>(Lf, t, y);
+      Sp.stv(Sp.Y, base + o, y);
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- pass 1 ---
-template <int B, class Tio, class S, int P, bool BWD, int G, bool SM, bool CL>
+// RING: store every interior factor L_j into a per-thread shared-memory ring
+// (element e of step i at ring[(i * RE + e) * rnt + rtid]) so that pass 2
+// only substitutes; otherwise checkpoint every G steps for re-factoring.
+template <int B, class Tio, class S, int P, bool BWD, int G, bool SM, bool CL, bool RING = false>
 __device__ __forceinline__ void lpass1_body(const Grp<Tio, P>& x, const Wts<S>& w, const SepL<B, S, CL>& Sp, S* ck, int k,
-                                            int f, int sig) {
+                                            int f, int sig, S* ring = nullptr, int rnt = 0, int rtid = 0) {
+  constexpr int RE = B * (B + 1) / 2 + B;
   const int T = x.T, l = sig - 1;
   S ap[2 * B - 1];
   if (f > 0) spow<B, S>(ldl<S, Tio, P, SM>(x.s, f - 1), w.s2, ap); else zero<2 * B - 1, S>(ap);
@@ -464,6 +711,13 @@ __device__ __forceinline__ void lpass1_body(const Grp<Tio, P>& x, const Wts<S>& 
       const int b = lchol<B, S>(M, Lf);
       if (b) { bad |= b; badj = min(badj, f); }
       llsolve<B, S>(Lf, rhs, wv);
+      if (RING) {
+        int e = 0;
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int q = 0; q <= i; ++q) ring[(e++) * rnt + rtid] = Lf[i][q];
+      }
       if (k > 0) {  // X_f = L_f^{-1} N_{f-1}
         S NL[B][B];
         lN<B, S>(ap, NL);
@@ -498,6 +752,14 @@ __device__ __forceinline__ void lpass1_body(const Grp<Tio, P>& x, const Wts<S>& 
       const int b = lchol<B, S>(M, Lf);
       if (b) { bad |= b; badj = min(badj, j); }
       llsolve<B, S>(Lf, rhs, wv);
+      if (RING) {
+        S* rp = ring + (j - f) * RE * rnt + rtid;
+        int e = 0;
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int q = 0; q <= i; ++q) rp[(e++) * rnt] = Lf[i][q];
+      }
       if (k > 0) {  // spike X_j = -L_j^{-1} P X_{j-1}; carried with alternating sign sg
         S Y[B][B];
 #pragma unroll
@@ -527,7 +789,7 @@ __device__ __forceinline__ void lpass1_body(const Grp<Tio, P>& x, const Wts<S>& 
         }
       }
       const int done = j - f + 1;
-      if ((done % G) == 0 && j < l) {  // checkpoint: resume point of pass-2 segment done/G
+      if (!RING && (done % G) == 0 && j < l) {  // checkpoint: resume point of pass-2 segment done/G
         S* cp = ck + (done / G - 1) * CkN<B>::N * Sp.nt + (k - Sp.rank * Sp.nt);
         int e = 0;
 #pragma unroll
@@ -734,6 +996,135 @@ __device__ __forceinline__ void lpass2_body(const Grp<Tio, P>& x, const Wts<S>& 
   }
 }
 
+// Pass 2 with the interior factors stored by pass 1 (RING): forward
+// substitution with both separator corrections, then back substitution; no
+// re-factorisation.  The ring's w slots receive the forward-substituted rhs.
+template <int B, class Tio, class S, int P, bool BWD, bool SM, bool CL>
+__device__ __forceinline__ void lpass2r_body(const Grp<Tio, P>& x, const Wts<S>& w, const SepL<B, S, CL>& Sp,
+                                             S* ring, int rnt, int rtid, int k, int f, int sig, const Vec<B, S>& yLv,
+                                             const Vec<B, S>& yRv) {
+  constexpr int LN = B * (B + 1) / 2, RE = LN + B;
+  const int l = sig - 1;
+  S yR[B], yL[B], yfR[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) { yR[i] = yRv.v[i]; yL[i] = yLv.v[i]; }
+  zero<B, S>(yfR);
+  if (!BWD) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) stl<S, Tio, P, SM>(x.yout, x.nv, sig * B + i, yR[i]);
+  } else {
+    ldlv<B, S, Tio, P, SM>(x.yin, sig * B, yfR);
+    lpoint_grads<B, S, Tio, P, SM>(x, w, sig, yR, yfR);
+  }
+  S yn[B], yfn[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) { yn[i] = yR[i]; yfn[i] = yfR[i]; }
+  if (f < sig) {
+    S Lp[B][B], wp[B], ap[2 * B - 1];
+    zero<B, S>(Lp);
+    zero<B, S>(wp);
+    if (f > 0) spow<B, S>(ldl<S, Tio, P, SM>(x.s, f - 1), w.s2, ap); else zero<2 * B - 1, S>(ap);
+#pragma unroll 1
+    for (int j = f; j <= l; ++j) {  // forward substitution
+      S* rp = ring + (j - f) * RE * rnt + rtid;
+      S Lf[B][B], rhs[B], an[2 * B - 1];
+      int e = 0;
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int q = 0; q <= i; ++q) Lf[i][q] = rp[(e++) * rnt];
+      if (BWD) {
+        ldlv<B, S, Tio, P, SM>(x.gy, j * B, rhs);
+      } else {
+        S c[B];
+        ldlv<B, S, Tio, P, SM>(x.c, j * B, c);
+        const S wd = mul_(w.g2, ldl<S, Tio, P, SM>(x.d, j));
+#pragma unroll
+        for (int i = 0; i < B; ++i) rhs[i] = mul_(wd, c[i]);
+        if (j == 0) {
+#pragma unroll
+          for (int i = 0; i < B; ++i)
+            if (i < x.n_iv) rhs[i] = fma_(w.i2, ldg_l<S, Tio, P>(x.u, i), rhs[i]);
+        }
+      }
+      spow<B, S>(ldl<S, Tio, P, SM>(x.s, j), w.s2, an);
+      S N[B][B], t[B];
+      lN<B, S>(ap, N);
+      if (j == f) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) t[q] = yL[q];  // rhs -= N_{f-1} y_L (zero for k = 0)
+      } else {
+        lltsolve<B, S>(Lp, wp, t);  // rhs -= P~_{j-1} w_{j-1} = N_{j-1} L_{j-1}^{-T} w_{j-1}
+      }
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+#pragma unroll
+        for (int r = 0; r < B; ++r) rhs[q] = fnma_(N[q][r], t[r], rhs[q]);
+      if (j == l) {  // rhs -= N_l^T y_R
+        S NR[B][B], u[B];
+        lN<B, S>(an, NR);
+        lmatTvec<B, S>(NR, yR, u);
+#pragma unroll
+        for (int q = 0; q < B; ++q) rhs[q] = sub_(rhs[q], u[q]);
+      }
+      llsolve<B, S>(Lf, rhs, wp);
+#pragma unroll
+      for (int q = 0; q < B; ++q) rp[(LN + q) * rnt] = wp[q];
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+#pragma unroll
+        for (int r = 0; r <= q; ++r) Lp[q][r] = Lf[q][r];
+#pragma unroll
+      for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+    }
+#pragma unroll 1
+    for (int j = l; j >= f; --j) {  // back substitution
+      const S* rp = ring + (j - f) * RE * rnt + rtid;
+      S Lf[B][B], wj[B], yv[B], an[2 * B - 1];
+      int e = 0;
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int q = 0; q <= i; ++q) Lf[i][q] = rp[(e++) * rnt];
+#pragma unroll
+      for (int q = 0; q < B; ++q) wj[q] = rp[(LN + q) * rnt];
+      const S sj = ldl<S, Tio, P, SM>(x.s, j);
+      spow<B, S>(sj, w.s2, an);
+      if (j == l) {
+        lltsolve<B, S>(Lf, wj, yv);
+      } else {  // y_j = L^{-T} (w_j - L^{-1} N_j^T y_{j+1})
+        S Nj[B][B], v[B], u[B], t[B];
+        lN<B, S>(an, Nj);
+        lmatTvec<B, S>(Nj, yn, v);
+        llsolve<B, S>(Lf, v, u);
+#pragma unroll
+        for (int q = 0; q < B; ++q) t[q] = sub_(wj[q], u[q]);
+        lltsolve<B, S>(Lf, t, yv);
+      }
+      if (!BWD) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) stl<S, Tio, P, SM>(x.yout, x.nv, j * B + q, yv[q]);
+      } else {
+        S yf[B];
+        ldlv<B, S, Tio, P, SM>(x.yin, j * B, yf);
+        lpoint_grads<B, S, Tio, P, SM>(x, w, j, yv, yf);
+        if (x.gs.on) stl<S, Tio, P, SM>(x.gs, x.nv, j, lds<B, S>(an, yv, yf, yn, yfn));
+#pragma unroll
+        for (int q = 0; q < B; ++q) yfn[q] = yf[q];
+      }
+#pragma unroll
+      for (int q = 0; q < B; ++q) yn[q] = yv[q];
+    }
+  }
+  if (BWD && k > 0 && x.gs.on) {  // interval (sigma_{k-1}, first point of the chunk)
+    const int jm = f - 1;
+    S yfm[B], am[2 * B - 1];
+    ldlv<B, S, Tio, P, SM>(x.yin, jm * B, yfm);
+    spow<B, S>(ldl<S, Tio, P, SM>(x.s, jm), w.s2, am);
+    stl<S, Tio, P, SM>(x.gs, x.nv, jm, lds<B, S>(am, yL, yfm, yn, yfn));
+  }
+}
+
 // Out-of-line versions for the streaming kernel (keeps its register allocation per pass).
 template <int B, class Tio, class S, int P, bool BWD, int G, bool SM>
 __device__ __noinline__ void lpass1(const Grp<Tio, P> x, const Wts<S> w, SepL<B, S> Sp, S* ck, int k, int f,
@@ -749,27 +1140,57 @@ __device__ __noinline__ void lpass2(const Grp<Tio, P> x, const Wts<S> w, SepL<B,
 __device__ __forceinline__ int chunk_begin(int k, int T, int K) { return int((int64_t(k) * T) / K); }
 
 // ------------------------------------------------------------ the kernel ---
+template <int B, class S>
+__device__ __forceinline__ void write_dummy_sep(const SepL<B, S, false>& Sp, int i) {
+  S Id[B][B], Z[B][B], z[B];
+  zero<B, S>(Z);
+  zero<B, S>(z);
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < B; ++c) Id[r][c] = splat<S>(r == c ? 1.0 : 0.0);
+  Sp.st(Sp.D, i, Id);
+  Sp.st(Sp.Bc, i, Z);
+  Sp.st(Sp.Y2, i, Z);
+  Sp.stv(Sp.R, i, z);
+  Sp.stv(Sp.Y, i, z);
+}
+
+template <int B, class S>
+__device__ __forceinline__ PortW<S, B> carve_ports(S* p, int W) {
+  PortW<S, B> PW;
+  PW.D0 = p;
+  PW.TL = PW.D0 + W * B * B;
+  PW.TP = PW.TL + W * B * B;
+  PW.R0 = PW.TP + W * B * B;
+  PW.Y0 = PW.R0 + W * B;
+  PW.TZ = PW.Y0 + W * B;
+  return PW;
+}
+
 template <int B, class Tio, class S, bool BWD, int G>
 __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) fused_kernel(Args<Tio> a) {
   constexpr int P = LaneT<S>::P;
   unsigned char* smem_raw = smnn_dyn_smem;
   const int K = a.K;
+  const int nt = blockDim.x;  // separator slots (K real + dummies)
   SepL<B, S> Sp;
   Sp.D = reinterpret_cast<S*>(smem_raw);
-  Sp.Bc = Sp.D + B * B * K;
-  Sp.Y2 = Sp.Bc + B * B * K;
-  Sp.R = Sp.Y2 + B * B * K;
-  Sp.Y = Sp.R + B * K;
-  Sp.time = reinterpret_cast<int*>(Sp.Y + B * K);
-  Sp.fail = Sp.time + K;
+  Sp.Bc = Sp.D + B * B * nt;
+  Sp.Y2 = Sp.Bc + B * B * nt;
+  Sp.R = Sp.Y2 + B * B * nt;
+  Sp.Y = Sp.R + B * nt;
+  const PortW<S, B> PW = carve_ports<B, S>(Sp.Y + B * nt, nt >> 5);
+  Sp.time = reinterpret_cast<int*>(PW.TZ + (nt >> 5) * B);
+  Sp.fail = Sp.time + nt;
   Sp.K = K;
-  Sp.nt = K;
+  Sp.nt = nt;
   Sp.rank = 0;
   Sp.cs = 1;
   const Wts<S> w{splat<S>(a.wg2), splat<S>(a.wi2), splat<S>(a.ws2)};
   const int k = threadIdx.x;
   const int T = a.T;
-  S* ck = reinterpret_cast<S*>(a.ckpt) + size_t(blockIdx.x) * size_t(a.nseg_ck) * CkN<B>::N * K;
+  S* ck = reinterpret_cast<S*>(a.ckpt) + size_t(blockIdx.x) * size_t(a.nseg_ck) * CkN<B>::N * nt;
   const int64_t ngroups = (a.n_inst + P - 1) / P;
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     if (k < P) Sp.fail[k] = INT_MAX;
@@ -781,25 +1202,35 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) fused_kerne
     if (k < K) {
       Sp.time[k] = sig;
       lpass1<B, Tio, S, P, BWD, G, false>(x, w, Sp, ck, k, f, sig);
+    } else {
+      write_dummy_sep<B, S>(Sp, k);
     }
     __syncthreads();
+    S Dk[B][B], rk[B];
     if (k + 1 < K) {  // add the right neighbour's Schur terms A_ll, r_l
-      S D[B][B], Al[B][B], r[B], rl[B];
-      Sp.ld(Sp.D, k, D);
+      S Al[B][B], rl[B];
+      Sp.ld(Sp.D, k, Dk);
       Sp.ld(Sp.Y2, k + 1, Al);
-      Sp.ldv(Sp.R, k, r);
+      Sp.ldv(Sp.R, k, rk);
       Sp.ldv(Sp.Y, k + 1, rl);
 #pragma unroll
       for (int i = 0; i < B; ++i) {
-        r[i] = add_(r[i], rl[i]);
+        rk[i] = add_(rk[i], rl[i]);
 #pragma unroll
-        for (int q = 0; q < B; ++q) D[i][q] = add_(D[i][q], Al[i][q]);
+        for (int q = 0; q < B; ++q) Dk[i][q] = add_(Dk[i][q], Al[i][q]);
       }
-      Sp.st(Sp.D, k, D);
-      Sp.stv(Sp.R, k, r);
     }
     __syncthreads();
+    if (k + 1 < K) {
+      Sp.st(Sp.D, k, Dk);
+      Sp.stv(Sp.R, k, rk);
+    }
+    __syncthreads();
+#if SMNN_WARP_BCR
+    lbcr_warp<B, S, P>(Sp, PW, k, nt);
+#else
     lbcr<B, S, P, false>(Sp, k);
+#endif
     if (k < K) {
       Vec<B, S> yL, yR;
       Sp.ldv(Sp.Y, k, yR.v);
@@ -810,7 +1241,6 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) fused_kerne
     if (k < x.nv && a.info) a.info[g * P + k] = (Sp.fail[k] == INT_MAX) ? 0 : Sp.fail[k];
   }
 }
-
 
 // ======================================================================
 // Resident kernel: the instance's inputs are bulk-copied (TMA, cp.async.bulk)
@@ -824,7 +1254,8 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) fused_kerne
 
 struct RLayout {
   int nt, cs;                              // threads per CTA, CTAs per cluster
-  int off_c, off_d, off_s, off_g, off_y;   // data regions (bytes, 16-aligned)
+  int off_c, off_d, off_s, off_g, off_y;   // data regions of lane 0 (bytes, 16-aligned)
+  int lane;                                // byte stride between the lanes' data regions
   int off_sep, off_ck, off_bar;
 };
 
@@ -869,9 +1300,9 @@ struct Span {
 };
 
 template <int B, class Tio, class S, bool BWD, int G, bool CL>
-__global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) resident_kernel(Args<Tio> a, RLayout L) {
-  static_assert(LaneT<S>::P == 1, "resident kernel: one instance per lane");
-  constexpr int P = 1;
+__global__ void __launch_bounds__(SMNN_MAX_THREADS, (LaneT<S>::P == 1 ? SMNN_MIN_BLOCKS : 1))
+    resident_kernel(Args<Tio> a, RLayout L) {
+  constexpr int P = LaneT<S>::P;
   unsigned char* sm = smnn_dyn_smem;
   const int cs = L.cs, nt = L.nt, tid = threadIdx.x;
   const int rank = CL ? int(cooperative_groups::this_cluster().block_rank()) : 0;
@@ -883,7 +1314,8 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) resident_ke
   Sp.Y2 = Sp.Bc + B * B * nt;
   Sp.R = Sp.Y2 + B * B * nt;
   Sp.Y = Sp.R + B * nt;
-  Sp.time = reinterpret_cast<int*>(Sp.Y + B * nt);
+  const PortW<S, B> PW = carve_ports<B, S>(Sp.Y + B * nt, nt >> 5);
+  Sp.time = reinterpret_cast<int*>(PW.TZ + (nt >> 5) * B);
   Sp.fail = Sp.time + nt;
   Sp.K = K;
   Sp.nt = nt;
@@ -891,11 +1323,6 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) resident_ke
   Sp.cs = cs;
   S* ck = reinterpret_cast<S*>(sm + L.off_ck);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.off_bar);
-  Tio* rc = reinterpret_cast<Tio*>(sm + L.off_c);
-  Tio* rd = reinterpret_cast<Tio*>(sm + L.off_d);
-  Tio* rs = reinterpret_cast<Tio*>(sm + L.off_s);
-  Tio* rg = BWD ? reinterpret_cast<Tio*>(sm + L.off_g) : nullptr;
-  Tio* ry = BWD ? reinterpret_cast<Tio*>(sm + L.off_y) : nullptr;
   const Wts<S> w{splat<S>(a.wg2), splat<S>(a.wi2), splat<S>(a.ws2)};
   if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
@@ -906,44 +1333,71 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) resident_ke
   const int s0 = max(t0 - 1, 0), s1 = min(t1, T - 1);
   const int y0 = max(t0 - 1, 0);
   const int f = chunk_begin(k, T, K), sig = chunk_begin(k + 1, T, K) - 1;
+  constexpr int E = int(sizeof(Tio));
+  const int64_t ngroups = (a.n_inst + P - 1) / P;
 
-  for (int64_t inst = blockIdx.x / cs; inst < a.n_inst; inst += nclusters) {
-    const int64_t tb = inst * int64_t(T) * B, t1b = inst * int64_t(T), tsb = inst * int64_t(T - 1);
-    const Span<Tio> pc(a.coeffs + tb + t0 * B, (t1 - t0) * B);
-    const Span<Tio> pd(a.rhs + t1b + t0, t1 - t0);
-    const Span<Tio> ps(a.steps + tsb + s0, s1 - s0);
-    const Span<Tio> pg(BWD ? a.grad_y + tb + t0 * B : a.coeffs, BWD ? (t1 - t0) * B : 0);
-    const Span<Tio> py(BWD ? a.y_in + tb + y0 * B : a.coeffs, BWD ? (t1 - y0) * B : 0);
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes);
-      bulk_g2s(rc, pc.lo, pc.bytes, bar);
-      bulk_g2s(rd, pd.lo, pd.bytes, bar);
-      if (ps.bytes) bulk_g2s(rs, ps.lo, ps.bytes, bar);
-      if (BWD) {
-        bulk_g2s(rg, pg.lo, pg.bytes, bar);
-        bulk_g2s(ry, py.lo, py.bytes, bar);
-      }
-    }
+  for (int64_t g = blockIdx.x / cs; g < ngroups; g += nclusters) {
+    const int nv = (a.n_inst - g * P < P) ? int(a.n_inst - g * P) : P;
     Grp<Tio, P> x;  // streams as element offsets into shared memory
     x.T = T;
     x.n_iv = a.n_iv;
-    x.nv = 1;
-    const int oc = L.off_c / int(sizeof(Tio)) + pc.pre - t0 * B;
-    const int od = L.off_d / int(sizeof(Tio)) + pd.pre - t0;
-    const int os = L.off_s / int(sizeof(Tio)) + ps.pre - s0;
-    x.c.o[0] = oc; x.c.on = true;
-    x.d.o[0] = od; x.d.on = true;
-    x.s.o[0] = os; x.s.on = true;
-    x.u[0] = a.iv + inst * a.n_iv;
-    x.gy.o[0] = BWD ? L.off_g / int(sizeof(Tio)) + pg.pre - t0 * B : 0; x.gy.on = BWD;
-    x.yin.o[0] = BWD ? L.off_y / int(sizeof(Tio)) + py.pre - y0 * B : 0; x.yin.on = BWD;
-    x.yout.o[0] = oc; x.yout.on = !BWD;
-    x.gc.o[0] = oc; x.gc.on = BWD && a.g_coeffs;
-    x.gd.o[0] = od; x.gd.on = BWD && a.g_rhs;
-    x.gs.o[0] = os; x.gs.on = BWD && a.g_steps;
-    x.gu[0] = (BWD && a.g_iv) ? a.g_iv + inst * a.n_iv : nullptr; x.gu_on = BWD && a.g_iv;
-    if (tid == 0) Sp.fail[0] = INT_MAX;
+    x.nv = nv;
+    int pre_c[P], pre_d[P], pre_s[P];
+    const Tio* lo[P][5];
+    uint32_t nb[P][5];
+    uint32_t tx = 0;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const int64_t inst = g * P + (q < nv ? q : 0);
+      const int64_t tb = inst * int64_t(T) * B, t1b = inst * int64_t(T), tsb = inst * int64_t(T - 1);
+      const int lb = q * L.lane;
+      const Span<Tio> pc(a.coeffs + tb + t0 * B, (t1 - t0) * B);
+      const Span<Tio> pd(a.rhs + t1b + t0, t1 - t0);
+      const Span<Tio> ps(a.steps + tsb + s0, s1 - s0);
+      const Span<Tio> pg(BWD ? a.grad_y + tb + t0 * B : a.coeffs, BWD ? (t1 - t0) * B : 0);
+      const Span<Tio> py(BWD ? a.y_in + tb + y0 * B : a.coeffs, BWD ? (t1 - y0) * B : 0);
+      lo[q][0] = pc.lo; nb[q][0] = pc.bytes;
+      lo[q][1] = pd.lo; nb[q][1] = pd.bytes;
+      lo[q][2] = ps.lo; nb[q][2] = ps.bytes;
+      lo[q][3] = pg.lo; nb[q][3] = pg.bytes;
+      lo[q][4] = py.lo; nb[q][4] = py.bytes;
+      tx += pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes;
+      pre_c[q] = pc.pre;
+      pre_d[q] = pd.pre;
+      pre_s[q] = ps.pre;
+      const int oc = (L.off_c + lb) / E + pc.pre - t0 * B;
+      const int od = (L.off_d + lb) / E + pd.pre - t0;
+      const int os = (L.off_s + lb) / E + ps.pre - s0;
+      x.c.o[q] = oc;
+      x.d.o[q] = od;
+      x.s.o[q] = os;
+      x.u[q] = a.iv + inst * a.n_iv;
+      x.gy.o[q] = BWD ? (L.off_g + lb) / E + pg.pre - t0 * B : 0;
+      x.yin.o[q] = BWD ? (L.off_y + lb) / E + py.pre - y0 * B : 0;
+      x.yout.o[q] = oc;
+      x.gc.o[q] = oc;
+      x.gd.o[q] = od;
+      x.gs.o[q] = os;
+      x.gu[q] = (BWD && a.g_iv) ? a.g_iv + inst * a.n_iv : nullptr;
+    }
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, tx);
+      const int offs[5] = {L.off_c, L.off_d, L.off_s, L.off_g, L.off_y};
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+          if (nb[q][r]) bulk_g2s(sm + offs[r] + q * L.lane, lo[q][r], nb[q][r], bar);
+    }
+    x.c.on = x.d.on = x.s.on = true;
+    x.gy.on = x.yin.on = BWD;
+    x.yout.on = !BWD;
+    x.gc.on = BWD && a.g_coeffs;
+    x.gd.on = BWD && a.g_rhs;
+    x.gs.on = BWD && a.g_steps;
+    x.gu_on = BWD && a.g_iv;
+    if (tid < P) Sp.fail[tid] = INT_MAX;
     Sp.time[tid] = sig;
     mbar_wait(bar, parity);
     parity ^= 1u;
@@ -972,7 +1426,11 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) resident_ke
       Sp.stv(Sp.R, k, rk);
     }
     Sp.sync();
+#if SMNN_WARP_BCR
+    if constexpr (CL) lbcr<B, S, P, CL>(Sp, k); else lbcr_warp<B, S, P>(Sp, PW, k, nt);
+#else
     lbcr<B, S, P, CL>(Sp, k);
+#endif
     Vec<B, S> yL, yR;
     Sp.ldv(Sp.Y, k, yR.v);
     if (k > 0) Sp.ldv(Sp.Y, k - 1, yL.v); else zero<B, S>(yL.v);
@@ -980,29 +1438,39 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) resident_ke
     lpass2_body<B, Tio, S, P, BWD, G, true, CL>(x, w, Sp, ck, k, f, sig, yL, yR);
     __syncthreads();
     // write the outputs back (coalesced)
-    if (!BWD) {
-      Tio* dst = a.y_out + tb + t0 * B;
-      for (int e = tid; e < (t1 - t0) * B; e += nt) dst[e] = rc[pc.pre + e];
-    } else {
-      if (a.g_coeffs) {
-        Tio* dst = a.g_coeffs + tb + t0 * B;
-        for (int e = tid; e < (t1 - t0) * B; e += nt) dst[e] = rc[pc.pre + e];
-      }
-      if (a.g_rhs) {
-        Tio* dst = a.g_rhs + t1b + t0;
-        for (int e = tid; e < t1 - t0; e += nt) dst[e] = rd[pd.pre + e];
-      }
-      if (a.g_steps) {  // this CTA owns intervals [s0, t1 - 1)
-        Tio* dst = a.g_steps + tsb + s0;
-        for (int e = tid; e < t1 - 1 - s0; e += nt) dst[e] = rs[ps.pre + e];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      if (q >= nv) break;
+      const int64_t inst = g * P + q;
+      const int64_t tb = inst * int64_t(T) * B, t1b = inst * int64_t(T), tsb = inst * int64_t(T - 1);
+      const Tio* rc = reinterpret_cast<const Tio*>(sm + L.off_c + q * L.lane) + pre_c[q];
+      const Tio* rd = reinterpret_cast<const Tio*>(sm + L.off_d + q * L.lane) + pre_d[q];
+      const Tio* rs = reinterpret_cast<const Tio*>(sm + L.off_s + q * L.lane) + pre_s[q];
+      if (!BWD) {
+        Tio* dst = a.y_out + tb + t0 * B;
+        for (int e = tid; e < (t1 - t0) * B; e += nt) dst[e] = rc[e];
+      } else {
+        if (a.g_coeffs) {
+          Tio* dst = a.g_coeffs + tb + t0 * B;
+          for (int e = tid; e < (t1 - t0) * B; e += nt) dst[e] = rc[e];
+        }
+        if (a.g_rhs) {
+          Tio* dst = a.g_rhs + t1b + t0;
+          for (int e = tid; e < t1 - t0; e += nt) dst[e] = rd[e];
+        }
+        if (a.g_steps) {  // this CTA owns intervals [s0, t1 - 1)
+          Tio* dst = a.g_steps + tsb + s0;
+          for (int e = tid; e < t1 - 1 - s0; e += nt) dst[e] = rs[e];
+        }
       }
     }
     Sp.sync();
-    if (rank == 0 && tid == 0 && a.info) {
-      int fv = Sp.fail[0];
+    if (rank == 0 && tid < nv && a.info) {
+      int fv = Sp.fail[tid];
       if (CL)
-        for (int r = 1; r < cs; ++r) fv = min(fv, *cooperative_groups::this_cluster().map_shared_rank(Sp.fail, r));
-      a.info[inst] = (fv == INT_MAX) ? 0 : fv;
+        for (int r = 1; r < cs; ++r)
+          fv = min(fv, *cooperative_groups::this_cluster().map_shared_rank(Sp.fail + tid, r));
+      a.info[g * P + tid] = (fv == INT_MAX) ? 0 : fv;
     }
     Sp.sync();
   }

@@ -323,7 +323,7 @@ int chunk_target() {
   static int m = 0;
   if (m == 0) {
     const char* e = std::getenv("SMNN_CHUNK");
-    m = e ? std::max(2, std::atoi(e)) : 16;
+    m = e ? std::max(2, std::atoi(e)) : 8;
   }
   return m;
 }
@@ -343,8 +343,14 @@ int threads_per_inst(const smnn_problem* p) {
 
 int chunks(const smnn_problem* p) { return std::min(threads_per_inst(p), p->T); }
 
+size_t ports_bytes(const smnn_problem* p, int nt) {  // per-warp scratch of the warp-tiled BCR
+  const int B = p->order + 1;
+  return size_t(nt / 32) * (3 * B * B + 3 * B) * lane_info(p).bytes;
+}
+
 size_t fused_smem(const smnn_problem* p) {
-  return sep_bytes_per_chunk(p) * chunks(p) + 4 * sizeof(int) + 16;
+  const int nt = threads_per_inst(p);
+  return sep_bytes_per_chunk(p) * nt + ports_bytes(p, nt) + 4 * sizeof(int) + 16;
 }
 
 int nseg_ck(const smnn_problem* p) {
@@ -424,7 +430,7 @@ int grid_blocks(const smnn_problem* p) {
 }
 
 size_t workspace_bytes(const smnn_problem* p) {
-  const size_t per = size_t(nseg_ck(p)) * ck_elems(p) * chunks(p) * lane_info(p).bytes;
+  const size_t per = size_t(nseg_ck(p)) * ck_elems(p) * threads_per_inst(p) * lane_info(p).bytes;
   return std::max<size_t>(per * grid_blocks(p), 256);
 }
 
@@ -492,14 +498,19 @@ RPlan resident_plan(const smnn_problem* p, bool bwd) {
       smnn::RLayout L{};
       L.nt = nt;
       L.cs = cs;
+      constexpr int P = smnn::LaneT<S>::P;
       size_t off = 0;
       auto take = [&](size_t bytes) { const size_t o = off; off = al16(off + bytes); return int(o); };
+      // per-lane data block: c, d, s (+ g, y backward); lanes repeat it P times
       L.off_c = take(size_t(Lmax) * B * es + 32);
       L.off_d = take(size_t(Lmax) * es + 32);
       L.off_s = take(size_t(Lmax + 1) * es + 32);
       L.off_g = bwd ? take(size_t(Lmax) * B * es + 32) : 0;
       L.off_y = bwd ? take(size_t(Lmax + 1) * B * es + 32) : 0;
-      L.off_sep = take(size_t(3 * B * B + 2 * B) * nt * ls + size_t(nt + 4) * 4);
+      L.lane = int(off);
+      off *= P;
+      L.off_sep = take(size_t(3 * B * B + 2 * B) * nt * ls + size_t(nt / 32) * (3 * B * B + 3 * B) * ls +
+                       size_t(nt + 4) * 4);
       const int nck = std::max(0, (maxchunk - 1 + G - 1) / G - 1);
       L.off_ck = take(size_t(nck) * smnn::CkN<B>::N * nt * ls + 16);
       L.off_bar = take(16);
@@ -550,7 +561,7 @@ int launch_resident(const smnn_problem* p, const smnn::Args<Tio>& a, const RPlan
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = nclusters;
   }
-  const int64_t nc = std::min<int64_t>(p->n_inst, nclusters);
+  const int64_t nc = std::min<int64_t>(n_groups(p), nclusters);
   cfg.gridDim = dim3(unsigned(nc * rp.L.cs));
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, rp.L);
   return check_cuda(e == cudaSuccess ? cudaGetLastError() : e, "resident kernel launch");
@@ -559,10 +570,8 @@ int launch_resident(const smnn_problem* p, const smnn::Args<Tio>& a, const RPlan
 template <int B, class Tio, class Tc, bool BWD>
 int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
   using S = typename smnn::LaneOf<Tio, Tc>::S;
-  if (smnn::LaneT<S>::P == 1) {
-    const RPlan rp = resident_plan<B, Tio, S>(p, BWD);
-    if (rp.ok) return launch_resident<B, Tio, Tc, BWD>(p, a, rp, st);
-  }
+  const RPlan rp = resident_plan<B, Tio, S>(p, BWD);
+  if (rp.ok) return launch_resident<B, Tio, Tc, BWD>(p, a, rp, st);
   const int nt = threads_per_inst(p);
   const size_t smem = fused_smem(p);
   const int grid = grid_blocks(p);
