@@ -1,8 +1,6 @@
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-SMNN_KERNEL=stream python -m pytest tests -m gpu -q -x -k "fused or full" 2>&1 | tail -2
-for wl in lorenz sst target; do
-for m in 8 16; do
-SMNN_CHUNK=$m python bench.py --workload $wl --steps 20 --no-cpu-baseline --e2e-steps 0 > gpurun_out/b.json 2>&1
-python -c "import json,sys; d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]); print('m=$m $wl', '%.3g' % d['value'], d['kernels_ms'], '%.3f' % d['roofline']['frac'])" 2>&1 | tail -1
-done; done
+# usage (on the GPU box): bash gpurun_prof.sh <tag> [workload]
+tag=${1:-rf}; wl=${2:-lorenz}
+python bench.py --workload $wl --steps 50 --no-cpu-baseline --e2e-steps 0 > gpurun_out/${tag}_bench.json 2>gpurun_out/${tag}_bench.err; tail -1 gpurun_out/${tag}_bench.json
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"rf_kernel|resident|fused" --csv --log-file gpurun_out/${tag}_launches.csv python bench.py --workload $wl --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"rf_kernel|resident|fused" -s 6 -c 2 -o gpurun_out/${tag}_prof python bench.py --workload $wl --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+ls gpurun_out | grep $tag

@@ -12,8 +12,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libsmnn.so")
-SOURCES = ["smnn_kernels.cu"]
-HEADERS = ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", os.path.join(ROOT, "include", "smnn.h")]
+SOURCES = ["smnn_kernels.cu", "smnn_rf.cu"]
+HEADERS = ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_rf.cuh", "smnn_rf_host.h", os.path.join(ROOT, "include", "smnn.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -29,27 +29,62 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+DEPS = {  # headers each translation unit includes
+    "smnn_kernels.cu": ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_rf_host.h"],
+    "smnn_rf.cu": ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_rf.cuh", "smnn_rf_host.h"],
+}
+
+
+def _obj(src: str) -> str:
+    return os.path.join(LIB_DIR, os.path.splitext(src)[0] + ".o")
+
+
+def _stale_obj(src: str) -> bool:
+    o = _obj(src)
+    if not os.path.exists(o):
+        return True
+    t = os.path.getmtime(o)
+    deps = [os.path.join(CSRC, src), os.path.join(ROOT, "include", "smnn.h"),
+            *[os.path.join(CSRC, h) for h in DEPS.get(src, HEADERS)]]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [
-        h if os.path.isabs(h) else os.path.join(CSRC, h) for h in HEADERS]
-    return any(os.path.getmtime(d) > t for d in deps)
+    return any(_stale_obj(s) or os.path.getmtime(_obj(s)) > t for s in SOURCES)
 
 
 def build_library(force: bool = False, verbose: bool = False, extra=()) -> str:
-    """Compile csrc/*.cu into lib/libsmnn.so (skipped when up to date)."""
+    """Compile csrc/*.cu (in parallel, one object each) and link lib/libsmnn.so (skipped when up to date)."""
     if not force and not _stale():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    procs, objs = [], []
+    for s in SOURCES:
+        obj = _obj(s)
+        objs.append(obj)
+        if not force and not _stale_obj(s):
+            continue
+        cmd = [nvcc(), *flags, *extra, *inc, "-c", "-o", obj, os.path.join(CSRC, s)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True), cmd))
+    errs = []
+    for pr, cmd in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            errs.append(" ".join(cmd) + "\n" + out + err)
+    if errs:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+           "-o", LIB + ".tmp", *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -309,7 +309,7 @@ __device__ __forceinline__ S lds(const S (&a)[2 * B - 1], const S (&lj)[B], cons
 // skip the level.  k is the caller's global thread index; all threads of the
 // block (cluster) must call it.
 template <int B, class S, int P, bool CL>
-__device__ __noinline__ void lbcr(SepL<B, S, CL> Sp, int k) {
+__device__ __forceinline__ void lbcr_body(const SepL<B, S, CL>& Sp, int k) {
   const int K = Sp.K;
   int hmax = 0;
 #pragma unroll 1
@@ -444,6 +444,11 @@ __device__ __noinline__ void lbcr(SepL<B, S, CL> Sp, int k) {
     }
     Sp.sync();
   }
+}
+
+template <int B, class S, int P, bool CL>
+__device__ __noinline__ void lbcr(SepL<B, S, CL> Sp, int k) {
+  lbcr_body<B, S, P, CL>(Sp, k);
 }
 
 // Warp-tiled two-ended block cyclic reduction (one CTA).  Separator i sits in

@@ -37,6 +37,7 @@
 #include "smnn.h"
 #include "smnn_device.cuh"
 #include "smnn_fused.cuh"
+#include "smnn_rf_host.h"
 
 #ifndef SMNN_F32_LANE
 #define SMNN_F32_LANE float
@@ -396,6 +397,13 @@ int occupancy(Kern kernel, int nt, size_t smem) {
   int occ = 1;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, smem);
+  {  // keep the attribute at the largest request (a smaller one may have lowered it)
+    static std::map<const void*, size_t> top;
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    size_t& t = top[reinterpret_cast<const void*>(kernel)];
+    t = std::max(t, smem);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(t));
+  }
   occ = std::max(occ, 1);
   std::lock_guard<std::mutex> lk(g_occ_mu);
   g_occ[key] = occ;
@@ -583,6 +591,12 @@ int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
 
 template <class Tio, class Tc, bool BWD>
 int dispatch_fused(const smnn_problem* p, const smnn::Args<Tio>& a, cudaStream_t st) {
+  {  // register-factor resident kernel first (smnn_rf.cuh); falls through when not eligible
+    std::string err;
+    const int r = smnn::rf_launch<Tio, Tc>(p, a, BWD, st, err);
+    if (r < 0) { g_err = err; return r; }
+    if (r == 1) return SMNN_OK;
+  }
   switch (p->order) {
     case 0: return launch_fused<1, Tio, Tc, BWD>(p, a, st);
     case 1: return launch_fused<2, Tio, Tc, BWD>(p, a, st);

@@ -19,18 +19,25 @@ template <> struct LaneT<double> { using T = double; static constexpr int P = 1;
 template <> struct LaneT<float2> { using T = float; static constexpr int P = 2; };
 template <> struct LaneT<double2> { using T = double; static constexpr int P = 2; };
 
-// ---- scalar
-__device__ __forceinline__ float fma_(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-__device__ __forceinline__ double fma_(double a, double b, double c) { return __fma_rn(a, b, c); }
-__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+// ---- scalar (plain operators: lets the compiler fold the +-1 / +-2 constants of
+// Appendix A.1 into neighbouring FFMAs; rounding stays IEEE round-to-nearest)
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float mul_(float a, float b) { return a * b; }
+__device__ __forceinline__ double mul_(double a, double b) { return a * b; }
+__device__ __forceinline__ float add_(float a, float b) { return a + b; }
+__device__ __forceinline__ double add_(double a, double b) { return a + b; }
 __device__ __forceinline__ float neg_(float a) { return -a; }
 __device__ __forceinline__ double neg_(double a) { return -a; }
-__device__ __forceinline__ float rsq_(float a) { return rsqrtf(a); }
+// MUFU.RSQ without the denormal-input fix-up sequence of rsqrtf (a pivot below
+// FLT_MIN is a breakdown anyway and is reported through `bad_`).
+__device__ __forceinline__ float rsq_(float a) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
 __device__ __forceinline__ double rsq_(double a) { return rsqrt(a); }
-__device__ __forceinline__ int bad_(float a) { return a > 0.f ? 0 : 1; }   // NaN -> bad
+__device__ __forceinline__ int bad_(float a) { return a >= 1.17549435e-38f ? 0 : 1; }   // NaN, <= 0, denormal -> bad
 __device__ __forceinline__ int bad_(double a) { return a > 0.0 ? 0 : 1; }
 
 // ---- packed fp32 (FFMA2 / FMUL2 / FADD2)
@@ -38,8 +45,8 @@ __device__ __forceinline__ float2 fma_(float2 a, float2 b, float2 c) { return __
 __device__ __forceinline__ float2 mul_(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 add_(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 neg_(float2 a) { return make_float2(-a.x, -a.y); }
-__device__ __forceinline__ float2 rsq_(float2 a) { return make_float2(rsqrtf(a.x), rsqrtf(a.y)); }
-__device__ __forceinline__ int bad_(float2 a) { return (a.x > 0.f ? 0 : 1) | (a.y > 0.f ? 0 : 2); }
+__device__ __forceinline__ float2 rsq_(float2 a) { return make_float2(rsq_(a.x), rsq_(a.y)); }
+__device__ __forceinline__ int bad_(float2 a) { return bad_(a.x) | (bad_(a.y) << 1); }
 
 // ---- two fp64 chains
 __device__ __forceinline__ double2 fma_(double2 a, double2 b, double2 c) {

@@ -1,0 +1,136 @@
+// smnn_rf.cu -- host side of the register-factor resident kernel (smnn_rf.cuh).
+//
+// Separate translation unit so the library's kernels compile in parallel;
+// smnn_kernels.cu calls rf_launch<Tio, Tc>() first and falls back to the
+// checkpointing kernels when the problem is not eligible.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "smnn.h"
+#include "smnn_rf.cuh"
+#include "smnn_rf_host.h"
+
+namespace smnn {
+namespace {
+
+size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+int sms() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    v = n;
+  }
+  return v;
+}
+
+bool rf_disabled() {
+  const char* e = std::getenv("SMNN_KERNEL");
+  return e && std::string(e) != "rf" && std::string(e) != "auto";
+}
+
+// Chunks (= threads) per instance: the fewest multiple-of-32 count whose
+// chunks hold at most CM points, with every chunk >= 2 points (an interior).
+int rf_threads(const smnn_problem* p, int CM) {
+  int nt = p->threads_per_inst;
+  if (nt == 0) {
+    nt = (p->T + CM - 1) / CM;
+    nt = ((nt + 31) / 32) * 32;
+  }
+  if (nt < 32 || nt > SMNN_RF_MAX_THREADS) return 0;
+  if (2 * nt > p->T) return 0;                       // every chunk needs an interior point
+  if ((p->T + nt - 1) / nt > CM) return 0;           // longest chunk must fit the registers
+  return nt;
+}
+
+template <int B, class Tio, class S, bool BWD>
+int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
+  constexpr int CM = RfCM<B, S>::value;
+  const int nt = rf_threads(p, CM);
+  if (nt == 0) return 0;
+  const size_t es = sizeof(Tio), ls = sizeof(S);
+  const int T = p->T;
+  RLayout L{};
+  L.nt = nt;
+  L.cs = 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off = al16(off + bytes); return int(o); };
+  L.off_c = take(size_t(T) * B * es + 32);
+  L.off_d = take(size_t(T) * es + 32);
+  L.off_s = take(size_t(T) * es + 32);
+  L.off_g = BWD ? take(size_t(T) * B * es + 32) : 0;
+  L.off_y = BWD ? take(size_t(T) * B * es + 32) : 0;
+  L.lane = int(off);
+  L.off_sep = take(size_t(RfSep<B, SMNN_RF_SEP>::R::N) * nt * ls + size_t(nt + 4) * 4);
+  L.off_ck = 0;
+  L.off_bar = take(16);
+  const size_t smem = off;
+  if (smem > 200 * 1024) return 0;
+  auto kern = rf_kernel<B, Tio, S, BWD, CM>;
+  static std::mutex mu;
+  static std::map<std::tuple<int, size_t>, int> occ_cache;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ_cache.find(std::make_tuple(nt, smem));
+    if (it != occ_cache.end()) occ = it->second;
+  }
+  static size_t smem_set = 0;  // the attribute must cover the largest request so far
+  if (smem > smem_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    std::lock_guard<std::mutex> lk(mu);
+    smem_set = std::max(smem_set, smem);
+  }
+  if (occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem) != cudaSuccess || occ < 1) {
+      cudaGetLastError();
+      occ = 1;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    occ_cache[std::make_tuple(nt, smem)] = occ;
+  }
+  // one CTA per instance up to 2^31 - 1 (the block scheduler balances the tail);
+  // the kernel strides over instances beyond that
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p->n_inst, int64_t(INT32_MAX)));
+  (void)occ;
+  Args<Tio> aa = a;
+  aa.K = nt;
+  kern<<<unsigned(grid), nt, smem, st>>>(aa, L);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("rf kernel launch: ") + cudaGetErrorString(e);
+    return SMNN_ERR_CUDA;
+  }
+  return 1;
+}
+
+template <class Tio, class S, bool BWD>
+int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
+  switch (p->order) {
+    case 0: return launch_B<1, Tio, S, BWD>(p, a, st, err);
+    case 1: return launch_B<2, Tio, S, BWD>(p, a, st, err);
+    case 2: return launch_B<3, Tio, S, BWD>(p, a, st, err);
+    default: return launch_B<4, Tio, S, BWD>(p, a, st, err);
+  }
+}
+
+}  // namespace
+
+template <class Tio, class Tc>
+int rf_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err) {
+  if (rf_disabled()) return 0;
+  return bwd ? launch_order<Tio, Tc, true>(p, a, st, err) : launch_order<Tio, Tc, false>(p, a, st, err);
+}
+
+template int rf_launch<float, float>(const smnn_problem*, const Args<float>&, bool, cudaStream_t, std::string&);
+template int rf_launch<float, double>(const smnn_problem*, const Args<float>&, bool, cudaStream_t, std::string&);
+template int rf_launch<double, double>(const smnn_problem*, const Args<double>&, bool, cudaStream_t, std::string&);
+
+}  // namespace smnn

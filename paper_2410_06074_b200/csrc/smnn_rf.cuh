@@ -1,0 +1,949 @@
+// smnn_rf.cuh -- register-factor (RF) resident kernel of the S-MNN solve.
+//
+// One CTA solves one instance whose inputs fit in shared memory (bulk-copied
+// there by TMA, as in resident_kernel).  Thread k owns time chunk
+// [f_k, f_{k+1}), f_k = floor(k T / K), K = blockDim.x chunks of at most CM
+// points (CM compile-time); the chunk's last point sigma_k is a separator, the
+// points before it its interior (>= 1 point).  Compared with resident_kernel:
+//
+//  * the interior Cholesky factors L_j (Algorithm 3's loop)
+//    stay in REGISTERS between pass 1 and pass 2 (the chunk loop is fully
+//    unrolled over CM, so every factor has a compile-time register home):
+//    pass 2 is substitution only (Algorithm 4), with no
+//    re-factorisation and no checkpoints;
+//  * pass 2 forward-substitutes the right-hand side with both separator
+//    values known (w'_j = L_j^{-1}(beta_j - N_{j-1} L_{j-1}^{-T} w'_{j-1}),
+//    w'_f = L_f^{-1}(beta_f - N_{f-1} y_L)) and back-substitutes
+//    y_j = L_j^{-T}(w'_j - L_j^{-1} N_j^T y_{j+1}) from y_{sigma_k};
+//  * the separator block-cyclic reduction is inlined (no call boundary, so
+//    the factor registers are not spilled around it).
+// Everything else (Appendix A.1 assembly, the spike / Schur complement onto
+// the separators, the BCR, the Appendix A.1 gradient chain) is the algebra of
+// smnn_fused.cuh, shared with the other fused kernels.
+#pragma once
+
+#include "smnn_fused.cuh"
+
+namespace smnn {
+
+// Chunk capacity: factors of CM - 1 interior points live in registers
+// ((CM-1) * B(B+1)/2 values of S).
+template <int B, class S>
+struct RfCM {
+  static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 8 : B == 2 ? 6 : B == 3 ? 3 : 2)
+                                              : (B == 1 ? 16 : B == 2 ? 12 : B == 3 ? 8 : 5);
+};
+
+// Separator solver of the RF kernel: 2 = block cyclic reduction with the blocks
+// in registers (rbcr2, default), 1 = parallel cyclic reduction (rpcr; faster
+// but not backward stable), 0 = block cyclic reduction in shared memory (rbcr).
+#ifndef SMNN_RF_SEP
+#define SMNN_RF_SEP 2
+#endif
+
+#ifndef SMNN_RF_MAX_THREADS
+#define SMNN_RF_MAX_THREADS 512
+#endif
+
+// o = N(a) v and o = N(a)^T v with N_ik = -H_ik a_{i+k} (w_s^2 S**).
+template <int B, class S>
+__device__ __forceinline__ void rNv(const S (&a)[2 * B - 1], const S (&v)[B], S (&o)[B]) {
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    S acc = mul_(splat<S>(-Hc(i, 0)), mul_(a[i], v[0]));
+#pragma unroll
+    for (int q = 1; q < B; ++q) acc = fma_(splat<S>(-Hc(i, q)), mul_(a[i + q], v[q]), acc);
+    o[i] = acc;
+  }
+}
+template <int B, class S>
+__device__ __forceinline__ void rNtv(const S (&a)[2 * B - 1], const S (&v)[B], S (&o)[B]) {
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    S acc = mul_(splat<S>(-Hc(0, q)), mul_(a[q], v[0]));
+#pragma unroll
+    for (int i = 1; i < B; ++i) acc = fma_(splat<S>(-Hc(i, q)), mul_(a[i + q], v[i]), acc);
+    o[q] = acc;
+  }
+}
+
+template <int B, class S>
+__device__ __forceinline__ void rcopyL(const S (&src)[B][B], S (&dst)[B][B]) {
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int q = 0; q <= i; ++q) dst[i][q] = src[i][q];
+}
+
+// ------------------------------------------------------------------ BCR ---
+// Separator records, array of structures: separator i occupies N consecutive
+// S values at sep + i*N (N odd, so lanes that touch records h apart hit
+// different banks for odd h):  D (diagonal block, lower triangle used; the
+// Cholesky factor after elimination), Bc (coupling block (i, i-h); Y1 after
+// elimination), Y2, R (rhs; v after elimination), Y (solution).
+template <int B>
+struct RRec {
+  static constexpr int raw = 3 * B * B + 2 * B;
+  static constexpr int N = raw | 1;
+  static constexpr int D = 0, BC = B * B, Y2 = 2 * B * B, R = 3 * B * B, Y = 3 * B * B + B;
+};
+
+template <int B, class S>
+__device__ __forceinline__ void rld_low(const S* p, S (&m)[B][B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) m[r][c] = p[r * B + c];
+}
+template <int B, class S>
+__device__ __forceinline__ void rst_low(S* p, const S (&m)[B][B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) p[r * B + c] = m[r][c];
+}
+template <int B, class S>
+__device__ __forceinline__ void rld_full(const S* p, S (&m)[B][B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < B; ++c) m[r][c] = p[r * B + c];
+}
+template <int B, class S>
+__device__ __forceinline__ void rst_full(S* p, const S (&m)[B][B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < B; ++c) p[r * B + c] = m[r][c];
+}
+template <int B, class S>
+__device__ __forceinline__ void rld_v(const S* p, S (&v)[B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r) v[r] = p[r];
+}
+template <int B, class S>
+__device__ __forceinline__ void rst_v(S* p, const S (&v)[B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r) p[r] = v[r];
+}
+
+// Block cyclic reduction of the K separators (SPD block tridiagonal), the
+// algebra of lbcr_body on the record layout: level h eliminates o = h (mod 2h)
+// (Cholesky of D_o, Y1 = L^{-1} B_o, Y2 = L^{-1} B_{o+h}^T, v = L^{-1} r_o) and
+// updates the survivors e = 0 (mod 2h); back substitution
+// y_o = L_o^{-T}(v_o - Y1 y_{o-h} - Y2 y_{o+h}).  All K threads call it.
+template <int B, class S>
+__device__ __forceinline__ void rbcr(S* sep, const int* time, int* fail, int K, int k) {
+  using Q = RRec<B>;
+  constexpr int N = Q::N;
+  int hmax = 0;
+#pragma unroll 1
+  for (int h = 1; h < K; h <<= 1) {
+    hmax = h;
+    {
+      const int o = h + 2 * h * k;
+      if (o < K) {
+        S* po = sep + o * N;
+        S D[B][B], Lf[B][B], Bk[B][B], Y1[B][B], Y2[B][B], r[B], v[B];
+        rld_low<B, S>(po + Q::D, D);
+        const int bd = lchol<B, S>(D, Lf);
+        if (bd) report<1>(fail, bd, time[o]);
+        rld_full<B, S>(po + Q::BC, Bk);
+        lleft<B, S>(Lf, Bk, Y1);
+        if (o + h < K) {
+          S Bn[B][B], BnT[B][B];
+          rld_full<B, S>(sep + (o + h) * N + Q::BC, Bn);
+#pragma unroll
+          for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int j = 0; j < B; ++j) BnT[i][j] = Bn[j][i];
+          lleft<B, S>(Lf, BnT, Y2);
+        } else {
+          zero<B, S>(Y2);
+        }
+        rld_v<B, S>(po + Q::R, r);
+        llsolve<B, S>(Lf, r, v);
+        rst_low<B, S>(po + Q::D, Lf);
+        rst_full<B, S>(po + Q::BC, Y1);
+        rst_full<B, S>(po + Q::Y2, Y2);
+        rst_v<B, S>(po + Q::R, v);
+      }
+    }
+    __syncthreads();
+    {
+      const int e = 2 * h * k;
+      if (e < K) {
+        S* pe = sep + e * N;
+        S D[B][B], r[B];
+        rld_low<B, S>(pe + Q::D, D);
+        rld_v<B, S>(pe + Q::R, r);
+        if (e - h >= 0) {
+          const S* po = sep + (e - h) * N;
+          S Y2o[B][B], vo[B];
+          rld_full<B, S>(po + Q::Y2, Y2o);
+          rld_v<B, S>(po + Q::R, vo);
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+#pragma unroll
+            for (int j = 0; j <= i; ++j) {
+              S aD = D[i][j];
+#pragma unroll
+              for (int m = 0; m < B; ++m) aD = fnma_(Y2o[m][i], Y2o[m][j], aD);
+              D[i][j] = aD;
+            }
+            S ar = r[i];
+#pragma unroll
+            for (int m = 0; m < B; ++m) ar = fnma_(Y2o[m][i], vo[m], ar);
+            r[i] = ar;
+          }
+          if (e - 2 * h >= 0) {  // new coupling (e, e-2h) = -Y2_o^T Y1_o
+            S Y1o[B][B], nb[B][B];
+            rld_full<B, S>(po + Q::BC, Y1o);
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+              for (int j = 0; j < B; ++j) {
+                S aB = mul_(Y2o[0][i], Y1o[0][j]);
+#pragma unroll
+                for (int m = 1; m < B; ++m) aB = fma_(Y2o[m][i], Y1o[m][j], aB);
+                nb[i][j] = neg_(aB);
+              }
+            rst_full<B, S>(pe + Q::BC, nb);
+          }
+        }
+        if (e + h < K) {
+          const S* po = sep + (e + h) * N;
+          S Y1o[B][B], vo[B];
+          rld_full<B, S>(po + Q::BC, Y1o);
+          rld_v<B, S>(po + Q::R, vo);
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+#pragma unroll
+            for (int j = 0; j <= i; ++j) {
+              S aD = D[i][j];
+#pragma unroll
+              for (int m = 0; m < B; ++m) aD = fnma_(Y1o[m][i], Y1o[m][j], aD);
+              D[i][j] = aD;
+            }
+            S ar = r[i];
+#pragma unroll
+            for (int m = 0; m < B; ++m) ar = fnma_(Y1o[m][i], vo[m], ar);
+            r[i] = ar;
+          }
+        }
+        rst_low<B, S>(pe + Q::D, D);
+        rst_v<B, S>(pe + Q::R, r);
+      }
+    }
+    __syncthreads();
+  }
+  if (k == 0) {
+    S D[B][B], Lf[B][B], r[B], t[B], y[B];
+    rld_low<B, S>(sep + Q::D, D);
+    const int bd = lchol<B, S>(D, Lf);
+    if (bd) report<1>(fail, bd, time[0]);
+    rld_v<B, S>(sep + Q::R, r);
+    llsolve<B, S>(Lf, r, t);
+    lltsolve<B, S>(Lf, t, y);
+    rst_v<B, S>(sep + Q::Y, y);
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int h = hmax; h >= 1; h >>= 1) {
+    const int o = h + 2 * h * k;
+    if (o < K) {
+      const S* po = sep + o * N;
+      S Lf[B][B], Y1[B][B], v[B], yl[B], t[B], y[B];
+      rld_low<B, S>(po + Q::D, Lf);
+      rld_full<B, S>(po + Q::BC, Y1);
+      rld_v<B, S>(po + Q::R, v);
+      rld_v<B, S>(sep + (o - h) * N + Q::Y, yl);
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        S acc = v[i];
+#pragma unroll
+        for (int m = 0; m < B; ++m) acc = fnma_(Y1[i][m], yl[m], acc);
+        t[i] = acc;
+      }
+      if (o + h < K) {
+        S Y2[B][B], yr[B];
+        rld_full<B, S>(po + Q::Y2, Y2);
+        rld_v<B, S>(sep + (o + h) * N + Q::Y, yr);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+          S acc = t[i];
+#pragma unroll
+          for (int m = 0; m < B; ++m) acc = fnma_(Y2[i][m], yr[m], acc);
+          t[i] = acc;
+        }
+      }
+      lltsolve<B, S>(Lf, t, y);
+      rst_v<B, S>(sep + o * N + Q::Y, y);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ PCR ---
+// Parallel cyclic reduction of the K x K block-tridiagonal SPD separator
+// system, one separator per thread, its blocks kept in registers:
+//   D_i (diagonal), Bl_i = block (i, i-h), Cr_i = block (i, i+h), r_i.
+// Level h: every thread factors D_i = L_i L_i^T and publishes
+//   F_i = L_i^{-1} Bl_i,  E_i = L_i^{-1} Cr_i,  g_i = L_i^{-1} r_i;
+// then eliminates its neighbours i -+ h from its own equation:
+//   D_i -= E_{i-h}^T E_{i-h} + F_{i+h}^T F_{i+h},  r_i -= E_{i-h}^T g_{i-h} + F_{i+h}^T g_{i+h},
+//   Bl_i = -E_{i-h}^T F_{i-h} (couples i-2h),  Cr_i = -F_{i+h}^T E_{i+h} (couples i+2h).
+// Each equation becomes a Schur complement of the SPD system, so every D_i
+// stays SPD; after ceil(log2 K) levels the system is block diagonal and
+// y_i = D_i^{-1} r_i.  The published triples alternate between two buffers,
+// so a level costs one barrier.  Record of separator i (PRec<B>::N values):
+// [buffer 0: F E g][buffer 1: F E g][y]; buffer 0 first carries the pass-1
+// hand-over (A_ll lower, A_rl, r_l) of the chunk to the right of the separator.
+template <int B>
+struct PRec {
+  static constexpr int W = 2 * B * B + B;
+  static constexpr int N = (2 * W + B) | 1;
+  static constexpr int F = 0, E = B * B, G = 2 * B * B, Y = 2 * W;
+  static constexpr int HA = F, HB = E, HR = G;  // pass-1 hand-over (buffer 0)
+};
+
+template <int B, class S>
+__device__ __forceinline__ void rpcr(S* rec, int K, int k, const int* stime, int* sfail, S (&D)[B][B],
+                                     S (&Bl)[B][B], S (&Cr)[B][B], S (&r)[B], S (&y)[B]) {
+  using Q = PRec<B>;
+  int bad = 0;
+  int lev = 0;
+#pragma unroll 1
+  for (int h = 1; h < K; h <<= 1, ++lev) {
+    const int bo = (lev & 1) ? 0 : Q::W;  // level 0 writes buffer 1 (buffer 0 holds the hand-over)
+    {
+      S Lf[B][B], F[B][B], E[B][B], gv[B];
+      bad |= lchol<B, S>(D, Lf);
+      lleft<B, S>(Lf, Bl, F);
+      lleft<B, S>(Lf, Cr, E);
+      llsolve<B, S>(Lf, r, gv);
+      S* pk = rec + k * Q::N + bo;
+      rst_full<B, S>(pk + Q::F, F);
+      rst_full<B, S>(pk + Q::E, E);
+      rst_v<B, S>(pk + Q::G, gv);
+    }
+    __syncthreads();
+    if (k - h >= 0) {
+      const S* pl = rec + (k - h) * Q::N + bo;
+      S El[B][B], Fl[B][B], gl[B];
+      rld_full<B, S>(pl + Q::E, El);
+      rld_full<B, S>(pl + Q::F, Fl);
+      rld_v<B, S>(pl + Q::G, gl);
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+          S a = D[i][j];
+#pragma unroll
+          for (int m = 0; m < B; ++m) a = fnma_(El[m][i], El[m][j], a);
+          D[i][j] = a;
+        }
+        S ar = r[i];
+#pragma unroll
+        for (int m = 0; m < B; ++m) ar = fnma_(El[m][i], gl[m], ar);
+        r[i] = ar;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          S a = mul_(El[0][i], Fl[0][j]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) a = fma_(El[m][i], Fl[m][j], a);
+          Bl[i][j] = neg_(a);
+        }
+      }
+    } else {
+      zero<B, S>(Bl);
+    }
+    if (k + h < K) {
+      const S* pr = rec + (k + h) * Q::N + bo;
+      S Fr[B][B], Er[B][B], gr[B];
+      rld_full<B, S>(pr + Q::F, Fr);
+      rld_full<B, S>(pr + Q::E, Er);
+      rld_v<B, S>(pr + Q::G, gr);
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+          S a = D[i][j];
+#pragma unroll
+          for (int m = 0; m < B; ++m) a = fnma_(Fr[m][i], Fr[m][j], a);
+          D[i][j] = a;
+        }
+        S ar = r[i];
+#pragma unroll
+        for (int m = 0; m < B; ++m) ar = fnma_(Fr[m][i], gr[m], ar);
+        r[i] = ar;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          S a = mul_(Fr[0][i], Er[0][j]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) a = fma_(Fr[m][i], Er[m][j], a);
+          Cr[i][j] = neg_(a);
+        }
+      }
+    } else {
+      zero<B, S>(Cr);
+    }
+  }
+  S Lf[B][B], t[B];
+  bad |= lchol<B, S>(D, Lf);
+  llsolve<B, S>(Lf, r, t);
+  lltsolve<B, S>(Lf, t, y);
+  if (bad) report<1>(sfail, bad, stime[k]);
+  rst_v<B, S>(rec + k * Q::N + Q::Y, y);
+  __syncthreads();
+}
+
+// ------------------------------------------------- BCR, registers resident ---
+// Block cyclic reduction with every separator's blocks in its thread's
+// registers (D, Bl = block (i, i-h), Cr = block (i, i+h), r).  At level h the
+// threads i = h (mod 2h) eliminate their separator -- D = L L^T, publish
+// L, F = L^{-1} Bl, E = L^{-1} Cr, g = L^{-1} r -- and after one barrier the
+// survivors i = 0 (mod 2h) update from their neighbours i -+ h:
+//   D -= E_{i-h}^T E_{i-h} + F_{i+h}^T F_{i+h},  r -= E_{i-h}^T g_{i-h} + F_{i+h}^T g_{i+h},
+//   Bl = -E_{i-h}^T F_{i-h},  Cr = -F_{i+h}^T E_{i+h}.
+// A separator publishes exactly once (when eliminated), so no buffer is
+// overwritten and a level costs one barrier.  Back substitution, one barrier
+// per level: y_i = L_i^{-T}(g_i - F_i y_{i-h} - E_i y_{i+h}).  This is the block
+// Cholesky factorisation of the odd-even permuted separator system (backward
+// stable), unlike PCR.  Record (BRec<B>::N values): L, F, E, g, y, then the
+// pass-1 hand-over (A_ll lower, A_rl, r_l) in slots of its own.
+template <int B>
+struct BRec {
+  static constexpr int L = 0, F = B * B, E = 2 * B * B, G = 3 * B * B, Y = 3 * B * B + B;
+  static constexpr int HA = 3 * B * B + 2 * B, HB = HA + B * B, HR = HA + 2 * B * B;
+  static constexpr int N = (5 * B * B + 3 * B) | 1;
+};
+
+template <int B, class S>
+__device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, int* sfail, S (&D)[B][B],
+                                      S (&Bl)[B][B], S (&Cr)[B][B], S (&r)[B]) {
+  using Q = BRec<B>;
+  int bad = 0;
+  int hmax = 1;
+  while (hmax < K) hmax <<= 1;
+  hmax >>= 1;  // largest level h < K (K >= 2)
+#pragma unroll 1
+  for (int h = 1; h < K; h <<= 1) {
+    const int m = k & (2 * h - 1);
+    if (m == h) {  // eliminate
+      S Lf[B][B], F[B][B], E[B][B], gv[B];
+      bad |= lchol<B, S>(D, Lf);
+      lleft<B, S>(Lf, Bl, F);
+      lleft<B, S>(Lf, Cr, E);
+      llsolve<B, S>(Lf, r, gv);
+      S* pk = rec + k * Q::N;
+      rst_low<B, S>(pk + Q::L, Lf);
+      rst_full<B, S>(pk + Q::F, F);
+      rst_full<B, S>(pk + Q::E, E);
+      rst_v<B, S>(pk + Q::G, gv);
+    }
+    __syncthreads();
+    if (m == 0) {  // survivor: absorb the eliminated neighbours
+      if (k - h >= 0) {
+        const S* pl = rec + (k - h) * Q::N;
+        S El[B][B], Fl[B][B], gl[B];
+        rld_full<B, S>(pl + Q::E, El);
+        rld_full<B, S>(pl + Q::F, Fl);
+        rld_v<B, S>(pl + Q::G, gl);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            S a = D[i][j];
+#pragma unroll
+            for (int q = 0; q < B; ++q) a = fnma_(El[q][i], El[q][j], a);
+            D[i][j] = a;
+          }
+          S ar = r[i];
+#pragma unroll
+          for (int q = 0; q < B; ++q) ar = fnma_(El[q][i], gl[q], ar);
+          r[i] = ar;
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            S a = mul_(El[0][i], Fl[0][j]);
+#pragma unroll
+            for (int q = 1; q < B; ++q) a = fma_(El[q][i], Fl[q][j], a);
+            Bl[i][j] = neg_(a);
+          }
+        }
+      }
+      if (k + h < K) {
+        const S* pr = rec + (k + h) * Q::N;
+        S Fr[B][B], Er[B][B], gr[B];
+        rld_full<B, S>(pr + Q::F, Fr);
+        rld_full<B, S>(pr + Q::E, Er);
+        rld_v<B, S>(pr + Q::G, gr);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            S a = D[i][j];
+#pragma unroll
+            for (int q = 0; q < B; ++q) a = fnma_(Fr[q][i], Fr[q][j], a);
+            D[i][j] = a;
+          }
+          S ar = r[i];
+#pragma unroll
+          for (int q = 0; q < B; ++q) ar = fnma_(Fr[q][i], gr[q], ar);
+          r[i] = ar;
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            S a = mul_(Fr[0][i], Er[0][j]);
+#pragma unroll
+            for (int q = 1; q < B; ++q) a = fma_(Fr[q][i], Er[q][j], a);
+            Cr[i][j] = neg_(a);
+          }
+        }
+      } else {
+        zero<B, S>(Cr);
+      }
+    }
+  }
+  if (k == 0) {  // the last survivor
+    S Lf[B][B], t[B], y[B];
+    bad |= lchol<B, S>(D, Lf);
+    llsolve<B, S>(Lf, r, t);
+    lltsolve<B, S>(Lf, t, y);
+    rst_v<B, S>(rec + Q::Y, y);
+  }
+  if (bad) report<1>(sfail, bad, stime[k]);
+#pragma unroll 1
+  for (int h = hmax; h >= 1; h >>= 1) {
+    __syncthreads();
+    if ((k & (2 * h - 1)) == h) {
+      const S* pk = rec + k * Q::N;
+      S Lf[B][B], F[B][B], yl[B], t[B], y[B];
+      rld_low<B, S>(pk + Q::L, Lf);
+      rld_full<B, S>(pk + Q::F, F);
+      rld_v<B, S>(pk + Q::G, t);
+      rld_v<B, S>(rec + (k - h) * Q::N + Q::Y, yl);
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int q = 0; q < B; ++q) t[i] = fnma_(F[i][q], yl[q], t[i]);
+      if (k + h < K) {
+        S E[B][B], yr[B];
+        rld_full<B, S>(pk + Q::E, E);
+        rld_v<B, S>(rec + (k + h) * Q::N + Q::Y, yr);
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int q = 0; q < B; ++q) t[i] = fnma_(E[i][q], yr[q], t[i]);
+      }
+      lltsolve<B, S>(Lf, t, y);
+      rst_v<B, S>(rec + k * Q::N + Q::Y, y);
+    }
+  }
+  __syncthreads();
+}
+
+template <int B, int SEP> struct RfSep { using R = BRec<B>; };
+template <int B> struct RfSep<B, 1> { using R = PRec<B>; };
+template <int B> struct RfSep<B, 0> { using R = RRec<B>; };
+
+template <class Tio>
+__device__ __forceinline__ void rf_store_out(Tio* dst, const Tio* src, int n, int tid, int nt) {
+  constexpr int E = int(sizeof(Tio));
+  const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst);
+  const uintptr_t ga = (g0 + 15) & ~uintptr_t(15), gb = (g0 + uintptr_t(n) * E) & ~uintptr_t(15);
+  const int head = int((ga - g0) / E);
+  const bool bulk = n * E >= 256 && gb > ga && ((smem_u32(src + head) & 15u) == 0u);
+  if (!bulk) {
+    for (int e = tid; e < n; e += nt) dst[e] = src[e];
+    return;
+  }
+  const int tail = head + int((gb - ga) / E);
+  if (tid < head) dst[tid] = src[tid];
+  if (tid < n - tail) dst[tail + tid] = src[tail + tid];
+  if (tid == 0)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
+                 "r"(smem_u32(src + head)), "r"(uint32_t(gb - ga))
+                 : "memory");
+}
+
+template <int B, class Tio, class S, bool BWD, int CM>
+__global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a, RLayout L) {
+  unsigned char* sm = smnn_dyn_smem;
+  Tio* smT = reinterpret_cast<Tio*>(sm);
+  const int nt = blockDim.x, k = threadIdx.x, K = nt;
+  const int T = a.T;
+  using Q = RRec<B>;
+  using R2 = typename RfSep<B, SMNN_RF_SEP>::R;
+  S* sep = reinterpret_cast<S*>(sm + L.off_sep);  // K separator records
+  int* stime = reinterpret_cast<int*>(sep + size_t(R2::N) * nt);
+  int* sfail = stime + nt;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.off_bar);
+  const Wts<S> w{splat<S>(a.wg2), splat<S>(a.wi2), splat<S>(a.ws2)};
+  if (k == 0) mbar_init(bar, 1);
+  __syncthreads();
+  uint32_t parity = 0;
+  const int f = chunk_begin(k, T, K), sig = chunk_begin(k + 1, T, K) - 1;
+  const int nint = sig - f;  // interior points, 1 <= nint <= CM - 1 (host guarantees)
+  constexpr int E = int(sizeof(Tio));
+
+  for (int64_t g = blockIdx.x; g < a.n_inst; g += gridDim.x) {
+    // ---- stage the instance (TMA bulk copies into shared memory)
+    const int64_t tb = g * int64_t(T) * B, t1b = g * int64_t(T), tsb = g * int64_t(T - 1);
+    const Span<Tio> pc(a.coeffs + tb, T * B);
+    const Span<Tio> pd(a.rhs + t1b, T);
+    const Span<Tio> ps(a.steps + tsb, T - 1);
+    const Span<Tio> pg(BWD ? a.grad_y + tb : a.coeffs, BWD ? T * B : 0);
+    const Span<Tio> py(BWD ? a.y_in + tb : a.coeffs, BWD ? T * B : 0);
+    if (k == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes);
+      bulk_g2s(sm + L.off_c, pc.lo, pc.bytes, bar);
+      bulk_g2s(sm + L.off_d, pd.lo, pd.bytes, bar);
+      if (ps.bytes) bulk_g2s(sm + L.off_s, ps.lo, ps.bytes, bar);
+      if (BWD) {
+        bulk_g2s(sm + L.off_g, pg.lo, pg.bytes, bar);
+        bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
+      }
+    }
+    Grp<Tio, 1> x;  // streams as element offsets into shared memory
+    x.T = T;
+    x.n_iv = a.n_iv;
+    x.nv = 1;
+    const int oc = L.off_c / E + pc.pre, od = L.off_d / E + pd.pre, os = L.off_s / E + ps.pre;
+    const int og = BWD ? L.off_g / E + pg.pre : 0, oy = BWD ? L.off_y / E + py.pre : 0;
+    x.c.o[0] = oc; x.d.o[0] = od; x.s.o[0] = os;
+    x.gy.o[0] = og; x.yin.o[0] = oy;
+    x.yout.o[0] = oc; x.gc.o[0] = oc; x.gd.o[0] = od; x.gs.o[0] = os;
+    x.u[0] = a.iv + g * a.n_iv;
+    x.gu[0] = (BWD && a.g_iv) ? a.g_iv + g * a.n_iv : nullptr;
+    x.c.on = x.d.on = x.s.on = true;
+    x.gy.on = x.yin.on = BWD;
+    x.yout.on = !BWD;
+    x.gc.on = BWD && a.g_coeffs;
+    x.gd.on = BWD && a.g_rhs;
+    x.gs.on = BWD && a.g_steps;
+    x.gu_on = BWD && a.g_iv;
+    // per-thread chunk views (immediate offsets from one base register each)
+    const Tio* cS = smT + oc + f * B;
+    const Tio* dS = smT + od + f;
+    const Tio* sS = smT + os + f;  // sS[-1] = s_{f-1}
+    const Tio* gS = smT + og + f * B;
+    if (k < 1) sfail[0] = INT_MAX;
+    stime[k] = sig;
+    mbar_wait(bar, parity);
+    parity ^= 1u;
+    __syncthreads();
+
+    // ================================================================ pass 1
+    S Lr[CM - 1][B][B];
+    S Dsep[B][B], Rsep[B];
+#if SMNN_RF_SEP != 0
+    S Bsep[B][B], Csep[B][B];
+#endif
+    {
+      S ap[2 * B - 1];
+      if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
+      S Lc[B][B], wv[B], X[B][B], All[B][B], rl[B];
+      zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
+      S sg = splat<S>(1.0);
+      int bad = 0, badj = INT_MAX;
+#pragma unroll
+      for (int i = 0; i < CM - 1; ++i) {
+        if (i < nint) {
+          S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
+#pragma unroll
+          for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
+          spow<B, S>(S(sS[i]), w.s2, an);
+          lassemble<B, S>(c, w.g2, ap, an, M, wc);
+          if (BWD) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
+          } else {
+            const S d = S(dS[i]);
+#pragma unroll
+            for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
+          }
+          if (i == 0 && k == 0) {  // initial-value rows at t = 0
+#pragma unroll
+            for (int r = 0; r < B; ++r)
+              if (r < x.n_iv) {
+                if (!BWD) rhs[r] = fma_(w.i2, S(x.u[0][r]), rhs[r]);
+                M[r][r] = add_(M[r][r], w.i2);
+              }
+          }
+          int b;
+          if (i == 0) {
+            b = lchol<B, S>(M, Lc);
+            llsolve<B, S>(Lc, rhs, wv);
+            S NL[B][B];  // spike X_f = L_f^{-1} N_{f-1} (zero for k = 0: ap = 0)
+            lN<B, S>(ap, NL);
+            lleft<B, S>(Lc, NL, X);
+#pragma unroll
+            for (int r = 0; r < B; ++r) {
+#pragma unroll
+              for (int q = 0; q <= r; ++q) {
+                S acc = mul_(X[0][r], X[0][q]);
+#pragma unroll
+                for (int m = 1; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
+                All[r][q] = acc;
+              }
+              S acc = mul_(X[0][r], wv[0]);
+#pragma unroll
+              for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
+              rl[r] = acc;
+            }
+          } else {
+            S Pm[B][B];
+            lPfromN<B, S>(ap, Lc, Pm);  // P_{j-1} = N_{j-1} L_{j-1}^{-T}
+            lcouple<B, S>(Pm, wv, M, rhs);
+            b = lchol<B, S>(M, Lc);
+            llsolve<B, S>(Lc, rhs, wv);
+            S Y[B][B];  // spike X_j = -L_j^{-1} P_{j-1} X_{j-1}, carried with sign sg
+#pragma unroll
+            for (int r = 0; r < B; ++r)
+#pragma unroll
+              for (int q = 0; q < B; ++q) {
+                S acc = mul_(Pm[r][0], X[0][q]);
+#pragma unroll
+                for (int m = 1; m < B; ++m) acc = fma_(Pm[r][m], X[m][q], acc);
+                Y[r][q] = acc;
+              }
+            lleft<B, S>(Lc, Y, X);
+            sg = neg_(sg);
+#pragma unroll
+            for (int r = 0; r < B; ++r) {
+#pragma unroll
+              for (int q = 0; q <= r; ++q) {
+                S acc = All[r][q];
+#pragma unroll
+                for (int m = 0; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
+                All[r][q] = acc;
+              }
+              S acc = mul_(X[0][r], wv[0]);
+#pragma unroll
+              for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
+              rl[r] = fma_(sg, acc, rl[r]);
+            }
+          }
+          if (b) { bad |= b; badj = min(badj, f + i); }
+          rcopyL<B, S>(Lc, Lr[i]);
+#pragma unroll
+          for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+        }
+      }
+      // Schur complement of the interior onto (sigma_{k-1}, sigma_k); ap = a(s_l).
+      S Pl[B][B], Arl[B][B];
+      lPfromN<B, S>(ap, Lc, Pl);
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          S a2 = mul_(Pl[r][0], X[0][q]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) a2 = fma_(Pl[r][m], X[m][q], a2);
+          Arl[r][q] = mul_(neg_(sg), a2);
+        }
+      }
+      // separator's own block and rhs (Appendix A.1) plus A_rr = -P_l P_l^T, r_r = -P_l w_l
+      {
+        S c[B], an[2 * B - 1], wc[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) c[r] = S(cS[nint * B + r]);
+        if (k + 1 < K) spow<B, S>(S(sS[nint]), w.s2, an); else zero<2 * B - 1, S>(an);
+        lassemble<B, S>(c, w.g2, ap, an, Dsep, wc);
+        if (BWD) {
+#pragma unroll
+          for (int r = 0; r < B; ++r) Rsep[r] = S(gS[nint * B + r]);
+        } else {
+          const S d = S(dS[nint]);
+#pragma unroll
+          for (int r = 0; r < B; ++r) Rsep[r] = mul_(wc[r], d);
+        }
+        lcouple<B, S>(Pl, wv, Dsep, Rsep);
+      }
+      // A_ll = -sum X^T X and r_l = -sum X^T w belong to sigma_{k-1}: hand them over.
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        rl[r] = neg_(rl[r]);
+#pragma unroll
+        for (int q = 0; q <= r; ++q) {
+          All[r][q] = neg_(All[r][q]);
+          All[q][r] = All[r][q];
+        }
+      }
+#if SMNN_RF_SEP == 0
+      S* pk = sep + k * Q::N;
+      rst_low<B, S>(pk + Q::Y2, All);
+      rst_v<B, S>(pk + Q::Y, rl);
+      rst_full<B, S>(pk + Q::BC, Arl);
+      if (bad) report<1>(sfail, bad, badj);
+    }
+    __syncthreads();
+    if (k + 1 < K) {  // add the right neighbour's A_ll, r_l
+      S Al[B][B], rr[B];
+      const S* pn = sep + (k + 1) * Q::N;
+      rld_low<B, S>(pn + Q::Y2, Al);
+      rld_v<B, S>(pn + Q::Y, rr);
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        Rsep[r] = add_(Rsep[r], rr[r]);
+#pragma unroll
+        for (int q = 0; q <= r; ++q) Dsep[r][q] = add_(Dsep[r][q], Al[r][q]);
+      }
+    }
+    // D / R are other fields of the record than the Y2 / Y the left neighbour reads
+    rst_low<B, S>(sep + k * Q::N + Q::D, Dsep);
+    rst_v<B, S>(sep + k * Q::N + Q::R, Rsep);
+    __syncthreads();
+    rbcr<B, S>(sep, stime, sfail, K, k);
+    S yL[B], yR[B];
+    rld_v<B, S>(sep + k * Q::N + Q::Y, yR);
+    if (k > 0) rld_v<B, S>(sep + (k - 1) * Q::N + Q::Y, yL); else zero<B, S>(yL);
+#else
+      S* pk = sep + k * R2::N;  // hand-over to separator k-1
+      rst_low<B, S>(pk + R2::HA, All);
+      rst_full<B, S>(pk + R2::HB, Arl);
+      rst_v<B, S>(pk + R2::HR, rl);
+      if (bad) report<1>(sfail, bad, badj);
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < B; ++q) Bsep[r][q] = Arl[r][q];
+    }
+    __syncthreads();
+    if (k + 1 < K) {  // the right chunk's A_ll, r_l and the coupling to sigma_{k+1}
+      S Al[B][B], An[B][B], rr[B];
+      const S* pn = sep + (k + 1) * R2::N;
+      rld_low<B, S>(pn + R2::HA, Al);
+      rld_full<B, S>(pn + R2::HB, An);
+      rld_v<B, S>(pn + R2::HR, rr);
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        Rsep[r] = add_(Rsep[r], rr[r]);
+#pragma unroll
+        for (int q = 0; q <= r; ++q) Dsep[r][q] = add_(Dsep[r][q], Al[r][q]);
+#pragma unroll
+        for (int q = 0; q < B; ++q) Csep[r][q] = An[q][r];
+      }
+    } else {
+      zero<B, S>(Csep);
+    }
+    S yL[B], yR[B];
+#if SMNN_RF_SEP == 1
+    __syncthreads();  // hand-over slots are PCR buffer 0
+    rpcr<B, S>(sep, K, k, stime, sfail, Dsep, Bsep, Csep, Rsep, yR);
+#else
+    rbcr2<B, S>(sep, K, k, stime, sfail, Dsep, Bsep, Csep, Rsep);
+    rld_v<B, S>(sep + k * R2::N + R2::Y, yR);
+#endif
+    if (k > 0) rld_v<B, S>(sep + (k - 1) * R2::N + R2::Y, yL); else zero<B, S>(yL);
+#endif
+
+    // ================================================================ pass 2
+    // forward substitution with both separator values known
+    S Wp[CM - 1][B];
+    {
+      S ap[2 * B - 1];
+      if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
+#pragma unroll
+      for (int i = 0; i < CM - 1; ++i) {
+        if (i < nint) {
+          S an[2 * B - 1], rhs[B], t[B], Nt[B];
+          spow<B, S>(S(sS[i]), w.s2, an);
+          if (BWD) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
+          } else {
+            const S d = S(dS[i]);
+#pragma unroll
+            for (int r = 0; r < B; ++r) rhs[r] = mul_(mul_(w.g2, S(cS[i * B + r])), d);
+            if (i == 0 && k == 0) {
+#pragma unroll
+              for (int r = 0; r < B; ++r)
+                if (r < x.n_iv) rhs[r] = fma_(w.i2, S(x.u[0][r]), rhs[r]);
+            }
+          }
+          if (i == 0) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) t[r] = yL[r];
+          } else {
+            lltsolve<B, S>(Lr[i - 1], Wp[i - 1], t);
+          }
+          rNv<B, S>(ap, t, Nt);
+#pragma unroll
+          for (int r = 0; r < B; ++r) rhs[r] = sub_(rhs[r], Nt[r]);
+          llsolve<B, S>(Lr[i], rhs, Wp[i]);
+#pragma unroll
+          for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+        }
+      }
+    }
+    // back substitution from y_{sigma_k}
+    {
+      S yn[B], yfn[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) yn[r] = yR[r];
+      zero<B, S>(yfn);
+      if (!BWD) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, sig * B + r, yR[r]);
+      } else {
+        ldlv<B, S, Tio, 1, true>(x.yin, sig * B, yfn);
+        lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR, yfn);
+      }
+#pragma unroll
+      for (int i = CM - 2; i >= 0; --i) {
+        if (i < nint) {
+          const int j = f + i;
+          S an[2 * B - 1], v[B], u[B], t[B], yv[B];
+          spow<B, S>(S(sS[i]), w.s2, an);
+          rNtv<B, S>(an, yn, v);
+          llsolve<B, S>(Lr[i], v, u);
+#pragma unroll
+          for (int r = 0; r < B; ++r) t[r] = sub_(Wp[i][r], u[r]);
+          lltsolve<B, S>(Lr[i], t, yv);
+          if (!BWD) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[r]);
+          } else {
+            S yf[B];
+            ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
+            lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv, yf);
+            if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv, yf, yn, yfn));
+#pragma unroll
+            for (int r = 0; r < B; ++r) yfn[r] = yf[r];
+          }
+#pragma unroll
+          for (int r = 0; r < B; ++r) yn[r] = yv[r];
+        }
+      }
+      if (BWD && k > 0 && x.gs.on) {  // interval (sigma_{k-1}, f)
+        S yfm[B], am[2 * B - 1];
+        ldlv<B, S, Tio, 1, true>(x.yin, (f - 1) * B, yfm);
+        spow<B, S>(S(sS[-1]), w.s2, am);
+        stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL, yfm, yn, yfn));
+      }
+    }
+    // ---- write the outputs back: TMA bulk store of the 16-byte aligned body,
+    //      plain stores for the unaligned head / tail elements
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    {
+      if (!BWD) {
+        rf_store_out(a.y_out + tb, smT + oc, T * B, k, nt);
+      } else {
+        if (a.g_coeffs) rf_store_out(a.g_coeffs + tb, smT + oc, T * B, k, nt);
+        if (a.g_rhs) rf_store_out(a.g_rhs + t1b, smT + od, T, k, nt);
+        if (a.g_steps) rf_store_out(a.g_steps + tsb, smT + os, T - 1, k, nt);
+      }
+      if (k == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (k == 0 && a.info) a.info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
+      // shared memory is reused (next instance) or released (exit) only after
+      // the bulk stores have read it
+      if (k == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace smnn

@@ -1,0 +1,22 @@
+// smnn_rf_host.h -- entry of the register-factor resident kernel (smnn_rf.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "smnn.h"
+
+namespace smnn {
+
+template <class Tio>
+struct Args;
+
+// Launches the RF kernel for `p` (forward or backward) when the problem fits
+// it (instance resident in shared memory, chunks within the register budget).
+// Returns 1 when launched, 0 when not eligible (caller falls back), or a
+// negative SMNN_ERR_* code with `err` set.
+template <class Tio, class Tc>
+int rf_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err);
+
+}  // namespace smnn
