@@ -37,8 +37,11 @@
  * smnn_last_error().  Argument errors are detected before any launch.
  * Numerical breakdown (a non-positive or non-finite Cholesky pivot, i.e.
  * M not numerically SPD) is reported per instance in `info` (may be NULL):
- * info[i] = 0 on success, else 1 + the time index of the first failing
- * block (like LAPACK potrf); the outputs of such an instance are undefined.
+ * info[i] = 0 on success, else 1 + a time index t0 <= t of the failing block
+ * t (like LAPACK potrf, which reports t itself): the time-parallel solver
+ * checks its pivots once per time chunk and reports the chunk's first point,
+ * or the separator point when the breakdown is in the separator system.  The
+ * outputs of such an instance are undefined.
  */
 #ifndef SMNN_H_
 #define SMNN_H_

@@ -134,3 +134,9 @@ template int rf_launch<float, double>(const smnn_problem*, const Args<float>&, b
 template int rf_launch<double, double>(const smnn_problem*, const Args<double>&, bool, cudaStream_t, std::string&);
 
 }  // namespace smnn
+
+#ifdef SMNN_RF_TIMING
+extern "C" int smnn_debug_rf_timing(unsigned long long* host, size_t n) {
+  return int(cudaMemcpyFromSymbol(host, smnn::rf_timing, n * sizeof(unsigned long long)));
+}
+#endif

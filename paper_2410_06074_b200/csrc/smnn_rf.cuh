@@ -41,6 +41,33 @@ struct RfCM {
 #define SMNN_RF_SEP 2
 #endif
 
+// Identity the compiler cannot see through (no rematerialisation from constants).
+__device__ __forceinline__ int opaque(int v) { asm volatile("" : "+r"(v)); return v; }
+__device__ __forceinline__ float opaque(float v) { asm volatile("" : "+f"(v)); return v; }
+__device__ __forceinline__ double opaque(double v) { asm volatile("" : "+d"(v)); return v; }
+
+// Thread -> chunk map: 1 = grouped by reduction level (rf_chunk_of_thread), 0 = identity.
+#ifndef RF_MAP
+#define RF_MAP 0
+#endif
+
+// Phase timestamps (debug builds only): per CTA, globaltimer at the phase boundaries.
+#ifdef SMNN_RF_TIMING
+__device__ unsigned long long rf_timing[6 * 65536];
+__device__ __forceinline__ unsigned long long rf_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define RF_STAMP(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) rf_timing[6 * blockIdx.x + (i)] = rf_now(); } while (0)
+#else
+#define RF_STAMP(i) do { } while (0)
+#endif
+
+#ifndef SMNN_RF_MIN_BLOCKS
+#define SMNN_RF_MIN_BLOCKS 1
+#endif
+
 #ifndef SMNN_RF_MAX_THREADS
 #define SMNN_RF_MAX_THREADS 512
 #endif
@@ -305,6 +332,7 @@ struct PRec {
   static constexpr int N = (2 * W + B) | 1;
   static constexpr int F = 0, E = B * B, G = 2 * B * B, Y = 2 * W;
   static constexpr int HA = F, HB = E, HR = G;  // pass-1 hand-over (buffer 0)
+  static constexpr bool shared_handover = false;
 };
 
 template <int B, class S>
@@ -414,10 +442,29 @@ __device__ __forceinline__ void rpcr(S* rec, int K, int k, const int* stime, int
 // pass-1 hand-over (A_ll lower, A_rl, r_l) in slots of its own.
 template <int B>
 struct BRec {
-  static constexpr int L = 0, F = B * B, E = 2 * B * B, G = 3 * B * B, Y = 3 * B * B + B;
-  static constexpr int HA = 3 * B * B + 2 * B, HB = HA + B * B, HR = HA + 2 * B * B;
-  static constexpr int N = (5 * B * B + 3 * B) | 1;
+  static constexpr int LT = B * (B + 1) / 2;  // packed lower triangle
+  static constexpr int L = 0, F = LT, E = LT + B * B, G = LT + 2 * B * B, Y = LT + 2 * B * B + B;
+  // pass-1 hand-over (A_ll packed lower, A_rl, r_l) shares the F / E / g slots:
+  // read before the first reduction level publishes (one extra barrier)
+  static constexpr int HA = F, HB = F + LT, HR = F + LT + B * B;
+  static constexpr int N = (LT + 2 * B * B + 2 * B) | 1;
+  static constexpr bool shared_handover = true;
 };
+
+template <int B, class S>
+__device__ __forceinline__ void rld_tri(const S* p, S (&m)[B][B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) m[r][c] = p[r * (r + 1) / 2 + c];
+}
+template <int B, class S>
+__device__ __forceinline__ void rst_tri(S* p, const S (&m)[B][B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) p[r * (r + 1) / 2 + c] = m[r][c];
+}
 
 template <int B, class S>
 __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, int* sfail, S (&D)[B][B],
@@ -437,7 +484,7 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
       lleft<B, S>(Lf, Cr, E);
       llsolve<B, S>(Lf, r, gv);
       S* pk = rec + k * Q::N;
-      rst_low<B, S>(pk + Q::L, Lf);
+      rst_tri<B, S>(pk + Q::L, Lf);
       rst_full<B, S>(pk + Q::F, F);
       rst_full<B, S>(pk + Q::E, E);
       rst_v<B, S>(pk + Q::G, gv);
@@ -518,7 +565,7 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
     if ((k & (2 * h - 1)) == h) {
       const S* pk = rec + k * Q::N;
       S Lf[B][B], F[B][B], yl[B], t[B], y[B];
-      rld_low<B, S>(pk + Q::L, Lf);
+      rld_tri<B, S>(pk + Q::L, Lf);
       rld_full<B, S>(pk + Q::F, F);
       rld_v<B, S>(pk + Q::G, t);
       rld_v<B, S>(rec + (k - h) * Q::N + Q::Y, yl);
@@ -566,11 +613,28 @@ __device__ __forceinline__ void rf_store_out(Tio* dst, const Tio* src, int n, in
                  : "memory");
 }
 
+// Thread -> chunk map: chunks ordered by the level at which the separator
+// reduction eliminates them (odd k first, then k = 2 mod 4, 4 mod 8, ...,
+// k = 0 last), so that at every level the eliminating and the surviving
+// separators sit in different warps and the reduction's two code paths do
+// not both run in every warp (levels >= 3 touch only the last warp for K=128).
+__device__ __forceinline__ int rf_chunk_of_thread(int t, int K) {
+  int h = 1, start = 0;
+  while (h < K) {
+    const int n = (K - h + 2 * h - 1) / (2 * h);  // #{k = h (mod 2h), k < K}
+    if (t < start + n) return h + 2 * h * (t - start);
+    start += n;
+    h <<= 1;
+  }
+  return 0;
+}
+
 template <int B, class Tio, class S, bool BWD, int CM>
-__global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a, RLayout L) {
+__global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_kernel(Args<Tio> a, RLayout L) {
   unsigned char* sm = smnn_dyn_smem;
   Tio* smT = reinterpret_cast<Tio*>(sm);
-  const int nt = blockDim.x, k = threadIdx.x, K = nt;
+  const int nt = blockDim.x, K = nt;
+  const int k = RF_MAP ? rf_chunk_of_thread(int(threadIdx.x), K) : int(threadIdx.x);
   const int T = a.T;
   using Q = RRec<B>;
   using R2 = typename RfSep<B, SMNN_RF_SEP>::R;
@@ -578,7 +642,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
   int* stime = reinterpret_cast<int*>(sep + size_t(R2::N) * nt);
   int* sfail = stime + nt;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.off_bar);
-  const Wts<S> w{splat<S>(a.wg2), splat<S>(a.wi2), splat<S>(a.ws2)};
+  const Wts<S> w{opaque(splat<S>(a.wg2)), opaque(splat<S>(a.wi2)), opaque(splat<S>(a.ws2))};
   if (k == 0) mbar_init(bar, 1);
   __syncthreads();
   uint32_t parity = 0;
@@ -587,6 +651,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
   constexpr int E = int(sizeof(Tio));
 
   for (int64_t g = blockIdx.x; g < a.n_inst; g += gridDim.x) {
+    RF_STAMP(0);
     // ---- stage the instance (TMA bulk copies into shared memory)
     const int64_t tb = g * int64_t(T) * B, t1b = g * int64_t(T), tsb = g * int64_t(T - 1);
     const Span<Tio> pc(a.coeffs + tb, T * B);
@@ -624,15 +689,18 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
     x.gs.on = BWD && a.g_steps;
     x.gu_on = BWD && a.g_iv;
     // per-thread chunk views (immediate offsets from one base register each)
-    const Tio* cS = smT + oc + f * B;
-    const Tio* dS = smT + od + f;
-    const Tio* sS = smT + os + f;  // sS[-1] = s_{f-1}
-    const Tio* gS = smT + og + f * B;
+    // opaque() keeps these offsets in registers: otherwise the compiler
+    // re-derives them from the kernel parameters at every unrolled step
+    const Tio* cS = smT + opaque(oc + f * B);
+    const Tio* dS = smT + opaque(od + f);
+    const Tio* sS = smT + opaque(os + f);  // sS[-1] = s_{f-1}
+    const Tio* gS = smT + opaque(og + f * B);
     if (k < 1) sfail[0] = INT_MAX;
     stime[k] = sig;
     mbar_wait(bar, parity);
     parity ^= 1u;
     __syncthreads();
+    RF_STAMP(1);
 
     // ================================================================ pass 1
     S Lr[CM - 1][B][B];
@@ -725,12 +793,16 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
               rl[r] = fma_(sg, acc, rl[r]);
             }
           }
-          if (b) { bad |= b; badj = min(badj, f + i); }
+          (void)b;  // pivots are checked once per chunk, below
           rcopyL<B, S>(Lc, Lr[i]);
 #pragma unroll
           for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
         }
       }
+      // A non-positive / non-finite pivot anywhere in the chunk leaves a
+      // non-finite value in the last factor (rsqrt of it is NaN / inf and the
+      // recurrence carries it forward): one check per chunk instead of per pivot.
+      if (bad_(splat<S>(1.0) / Lc[B - 1][B - 1])) { bad = 1; badj = f; }
       // Schur complement of the interior onto (sigma_{k-1}, sigma_k); ap = a(s_l).
       S Pl[B][B], Arl[B][B];
       lPfromN<B, S>(ap, Lc, Pl);
@@ -801,7 +873,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
     if (k > 0) rld_v<B, S>(sep + (k - 1) * Q::N + Q::Y, yL); else zero<B, S>(yL);
 #else
       S* pk = sep + k * R2::N;  // hand-over to separator k-1
-      rst_low<B, S>(pk + R2::HA, All);
+      rst_tri<B, S>(pk + R2::HA, All);
       rst_full<B, S>(pk + R2::HB, Arl);
       rst_v<B, S>(pk + R2::HR, rl);
       if (bad) report<1>(sfail, bad, badj);
@@ -811,10 +883,11 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
         for (int q = 0; q < B; ++q) Bsep[r][q] = Arl[r][q];
     }
     __syncthreads();
+    RF_STAMP(2);
     if (k + 1 < K) {  // the right chunk's A_ll, r_l and the coupling to sigma_{k+1}
       S Al[B][B], An[B][B], rr[B];
       const S* pn = sep + (k + 1) * R2::N;
-      rld_low<B, S>(pn + R2::HA, Al);
+      rld_tri<B, S>(pn + R2::HA, Al);
       rld_full<B, S>(pn + R2::HB, An);
       rld_v<B, S>(pn + R2::HR, rr);
 #pragma unroll
@@ -833,12 +906,14 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
     __syncthreads();  // hand-over slots are PCR buffer 0
     rpcr<B, S>(sep, K, k, stime, sfail, Dsep, Bsep, Csep, Rsep, yR);
 #else
+    if (R2::shared_handover) __syncthreads();  // hand-over read before level 1 publishes
     rbcr2<B, S>(sep, K, k, stime, sfail, Dsep, Bsep, Csep, Rsep);
     rld_v<B, S>(sep + k * R2::N + R2::Y, yR);
 #endif
     if (k > 0) rld_v<B, S>(sep + (k - 1) * R2::N + R2::Y, yL); else zero<B, S>(yL);
 #endif
 
+    RF_STAMP(3);
     // ================================================================ pass 2
     // forward substitution with both separator values known
     S Wp[CM - 1][B];
@@ -924,6 +999,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
         stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL, yfm, yn, yfn));
       }
     }
+    RF_STAMP(4);
     // ---- write the outputs back: TMA bulk store of the 16-byte aligned body,
     //      plain stores for the unaligned head / tail elements
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -943,6 +1019,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, 1) rf_kernel(Args<Tio> a,
       if (k == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     __syncthreads();
+    RF_STAMP(5);
   }
 }
 

@@ -185,7 +185,9 @@ def test_info_reports_breakdown(smnn):
     t = to_dev(x, torch.float64)
     _, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"])
     info = info.cpu().numpy()
-    assert info[0] == 0 and info[2] == 0 and info[1] > 0
+    # 1 + a time index at or before the failing block (the first point of the
+    # time chunk in which the breakdown was detected; include/smnn.h)
+    assert info[0] == 0 and info[2] == 0 and 1 <= info[1] <= 1 + 123
 
 
 def test_autograd_gradcheck(smnn):
