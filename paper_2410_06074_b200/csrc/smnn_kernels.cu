@@ -439,7 +439,7 @@ int grid_blocks(const smnn_problem* p) {
 
 size_t workspace_bytes(const smnn_problem* p) {
   const size_t per = size_t(nseg_ck(p)) * ck_elems(p) * threads_per_inst(p) * lane_info(p).bytes;
-  return std::max<size_t>(per * grid_blocks(p), 256);
+  return std::max<size_t>({per * grid_blocks(p), smnn::pipe_workspace_bytes(p), size_t(256)});
 }
 
 template <class Tio>
@@ -591,11 +591,23 @@ int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
 
 template <class Tio, class Tc, bool BWD>
 int dispatch_fused(const smnn_problem* p, const smnn::Args<Tio>& a, cudaStream_t st) {
-  {  // register-factor resident kernel first (smnn_rf.cuh); falls through when not eligible
+  {  // SMNN_KERNEL = auto (default) | pipe | rf | resident | stream
+    const char* env = std::getenv("SMNN_KERNEL");
+    const std::string mode = env ? env : "auto";
     std::string err;
-    const int r = smnn::rf_launch<Tio, Tc>(p, a, BWD, st, err);
-    if (r < 0) { g_err = err; return r; }
-    if (r == 1) return SMNN_OK;
+    // measured on B200: the resident RF kernel wins while one CTA holds the
+    // instance (T <~ 4k); the pipeline beyond (T = 1e4: 2.1x the streaming
+    // kernel), except fp64 arithmetic at order 3 (register spills)
+    if (mode == "auto" || mode == "rf") {  // register-factor resident kernel (smnn_rf.cuh)
+      const int r = smnn::rf_launch<Tio, Tc>(p, a, BWD, st, err);
+      if (r < 0) { g_err = err; return r; }
+      if (r == 1) return SMNN_OK;
+    }
+    if (mode == "pipe" || (mode == "auto" && !(sizeof(Tc) == 8 && p->order >= 3))) {  // smnn_pipe.cuh
+      const int r = smnn::pipe_launch<Tio, Tc>(p, a, BWD, st, err);
+      if (r < 0) { g_err = err; return r; }
+      if (r == 1) return SMNN_OK;
+    }
   }
   switch (p->order) {
     case 0: return launch_fused<1, Tio, Tc, BWD>(p, a, st);

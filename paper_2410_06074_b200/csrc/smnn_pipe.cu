@@ -1,0 +1,168 @@
+// smnn_pipe.cu -- host side of the three-kernel pipeline (smnn_pipe.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
+#include "smnn.h"
+#include "smnn_pipe.cuh"
+#include "smnn_rf_host.h"
+
+namespace smnn {
+namespace {
+
+size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct PipePlan {
+  bool ok = false;
+  int K = 0, NT = 0, parts = 0, CM = 0;
+  bool sep2 = false;  // separator kernel: pipe_sep2_kernel (128 threads, K/128 separators each)
+  size_t smem_p1 = 0, smem_p2 = 0, smem_sep = 0;
+  size_t ws_sep1 = 0, ws_ysep = 0, ws_fail = 0;
+  PipeL L1{}, L2{};
+};
+
+template <int B, class S>
+PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
+  PipePlan q;
+  constexpr int CM = PipeCM<B, S>::value;
+  const int T = p->T;
+  if (p->threads_per_inst != 0 || T < 4) return q;
+  // chunks: a multiple of 32 (no idle lanes in the chunk kernels), each of
+  // 2..CM points (chunk_begin spreads the remainder)
+  int K = std::min(((T + CM - 1) / CM + 31) / 32 * 32, T / 2);
+  if (K > 256) K = std::min((K + 127) / 128 * 128, T / 2);  // large K: 4 separators per thread (sep2)
+  if (K < 1 || K > SMNN_PIPE_SEP_MAX || (T + K - 1) / K > CM) return q;
+  q.sep2 = K > 256 && K % 128 == 0;
+  const size_t ls = sizeof(S);
+  q.K = K;
+  q.CM = CM;
+  q.NT = std::min(SMNN_PIPE_NT, ((K + 31) / 32) * 32);
+  q.parts = (K + q.NT - 1) / q.NT;
+  const int steps = q.NT * CM + 2;  // points of one CTA range (+ s_{ta-1}, y_{ta-1})
+  auto layout = [&](PipeL& L, bool p2) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off = al16(off + bytes); return int(o); };
+    L.off_c = take(size_t(steps) * B * es + 32);
+    L.off_d = (p2 || !bwd) ? take(size_t(steps) * es + 32) : 0;
+    L.off_s = take(size_t(steps) * es + 32);
+    L.off_g = bwd ? take(size_t(steps) * B * es + 32) : 0;
+    L.off_y = (bwd && p2) ? take(size_t(steps) * B * es + 32) : 0;
+    L.off_h = p2 ? 0 : take(size_t(PSep<B>::LT + B) * SMNN_PIPE_NT * ls);
+    L.off_bar = take(16);
+    return off;
+  };
+  q.smem_p1 = layout(q.L1, false);
+  q.smem_p2 = layout(q.L2, true);
+  q.smem_sep = size_t(BRec<B>::N) * (q.sep2 ? K / 4 : K) * ls + size_t(2 * K + 4) * 4;
+  if (q.smem_p1 > 200 * 1024 || q.smem_p2 > 200 * 1024 || q.smem_sep > 220 * 1024) return q;
+  q.ws_sep1 = al256(size_t(p->n_inst) * PSep<B>::N * K * ls);
+  q.ws_ysep = al256(size_t(p->n_inst) * B * K * ls);
+  q.ws_fail = al256(size_t(p->n_inst) * K * 4);
+  for (PipeL* L : {&q.L1, &q.L2}) {
+    L->K = K;
+    L->NT = q.NT;
+    L->parts = q.parts;
+    const char* e = std::getenv("SMNN_PIPE_SEPMAP");
+    L->sepmap = e ? std::atoi(e) : 1;
+  }
+  q.ok = true;
+  return q;
+}
+
+template <class S>
+PipePlan plan_S(const smnn_problem* p, size_t es, bool bwd) {
+  switch (p->order) {
+    case 0: return plan_B<1, S>(p, es, bwd);
+    case 1: return plan_B<2, S>(p, es, bwd);
+    case 2: return plan_B<3, S>(p, es, bwd);
+    default: return plan_B<4, S>(p, es, bwd);
+  }
+}
+
+PipePlan plan_of(const smnn_problem* p, bool bwd) {
+  if (p->dtype == SMNN_F32) return plan_S<float>(p, 4, bwd);
+  return plan_S<double>(p, p->dtype == SMNN_F64 ? 8 : 4, bwd);
+}
+
+template <class Kern>
+void set_smem(Kern k, size_t smem) {
+  static std::mutex mu;
+  static size_t top = 0;  // per kernel instantiation (template)
+  std::lock_guard<std::mutex> lk(mu);
+  if (smem > top) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    top = smem;
+  }
+}
+
+template <int B, class Tio, class S, bool BWD>
+int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
+  constexpr int CM = PipeCM<B, S>::value;
+  PipePlan q = plan_B<B, S>(p, sizeof(Tio), BWD);
+  if (!q.ok) return 0;
+  char* ws = static_cast<char*>(a.ckpt);
+  for (PipeL* L : {&q.L1, &q.L2}) {
+    L->sep1 = ws;
+    L->ysep = ws + q.ws_sep1;
+    L->cfail = reinterpret_cast<int*>(ws + q.ws_sep1 + q.ws_ysep);
+  }
+  const unsigned grid_c = unsigned(p->n_inst * q.parts);
+  auto k1 = pipe_p1_kernel<B, Tio, S, BWD, CM>;
+  auto k2 = pipe_sep_kernel<B, S>;
+  auto k2b = pipe_sep2_kernel<B, S, 4>;
+  auto k3 = pipe_p2_kernel<B, Tio, S, BWD, CM>;
+  set_smem(k1, q.smem_p1);
+  set_smem(k3, q.smem_p2);
+  k1<<<grid_c, q.NT, q.smem_p1, st>>>(a, q.L1);
+  if (q.sep2) {
+    set_smem(k2b, q.smem_sep);
+    k2b<<<unsigned(p->n_inst), q.K / 4, q.smem_sep, st>>>(q.L1, p->T, a.info);
+  } else {
+    set_smem(k2, q.smem_sep);
+    k2<<<unsigned(p->n_inst), q.K, q.smem_sep, st>>>(q.L1, p->T, a.info);
+  }
+  k3<<<grid_c, q.NT, q.smem_p2, st>>>(a, q.L2);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("pipeline launch: ") + cudaGetErrorString(e);
+    return SMNN_ERR_CUDA;
+  }
+  return 1;
+}
+
+template <class Tio, class S, bool BWD>
+int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
+  switch (p->order) {
+    case 0: return launch_B<1, Tio, S, BWD>(p, a, st, err);
+    case 1: return launch_B<2, Tio, S, BWD>(p, a, st, err);
+    case 2: return launch_B<3, Tio, S, BWD>(p, a, st, err);
+    default: return launch_B<4, Tio, S, BWD>(p, a, st, err);
+  }
+}
+
+}  // namespace
+
+size_t pipe_workspace_bytes(const smnn_problem* p) {
+  const PipePlan f = plan_of(p, false), b = plan_of(p, true);
+  size_t n = 0;
+  if (f.ok) n = std::max(n, f.ws_sep1 + f.ws_ysep + f.ws_fail);
+  if (b.ok) n = std::max(n, b.ws_sep1 + b.ws_ysep + b.ws_fail);
+  return n;
+}
+
+template <class Tio, class Tc>
+int pipe_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err) {
+  return bwd ? launch_order<Tio, Tc, true>(p, a, st, err) : launch_order<Tio, Tc, false>(p, a, st, err);
+}
+
+template int pipe_launch<float, float>(const smnn_problem*, const Args<float>&, bool, cudaStream_t, std::string&);
+template int pipe_launch<float, double>(const smnn_problem*, const Args<float>&, bool, cudaStream_t, std::string&);
+template int pipe_launch<double, double>(const smnn_problem*, const Args<double>&, bool, cudaStream_t,
+                                         std::string&);
+
+}  // namespace smnn

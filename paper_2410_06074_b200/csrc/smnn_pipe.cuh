@@ -1,0 +1,782 @@
+// smnn_pipe.cuh -- the S-MNN solve as a three-kernel pipeline.
+//
+// The time-parallel partition solver of smnn_rf.cuh split at its two
+// synchronisation points, so that the register-heavy chunk sweeps and the
+// latency-bound separator reduction no longer share one CTA's lifetime:
+//
+//   P1  chunk kernel: thread = time chunk [f_k, f_{k+1}); block Cholesky of the
+//       chunk interior with the spike (Algorithm 3's loop),
+//       Schur complement of the interior onto its two separators; writes the
+//       separator blocks to the workspace.  No barrier after staging.
+//   SEP separator kernel: CTA = instance, thread = separator; assembles the
+//       K x K block-tridiagonal Schur system and solves it by block cyclic
+//       reduction with the blocks in registers (rbcr2); writes y at the
+//       separators and info.
+//   P2  chunk kernel: re-factors the chunk interior in registers (forward
+//       sweep, with both separator values known) and back-substitutes
+//       (Algorithm 4); FWD writes y, BWD the Appendix A.1
+//       gradient chain.  No barrier after staging.
+//
+// The chunk kernels stage their CTA's time range with TMA bulk copies
+// (cp.async.bulk) and write outputs with TMA bulk stores, as the RF kernel.
+// Workspace (S = arithmetic type), per instance g and chunk / separator k,
+// field-major so that a warp's 32 consecutive chunks touch 128 contiguous
+// bytes per field:
+//   sep1 [g][PSep<B>::N][K]  D_own (lower, packed), R_own, A_rl, A_ll (packed), r_l
+//   ysep [g][B][K]           y at the separators
+//   cfail[g][K]              1 + first point of a chunk whose pivots broke down, else INT_MAX
+#pragma once
+
+#include "smnn_rf.cuh"
+
+namespace smnn {
+
+template <int B, class S>
+struct PipeCM {  // chunk capacity: P2 keeps CM - 1 factors + rhs in registers
+  static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 12 : B == 2 ? 8 : B == 3 ? 5 : 4)
+                                              : (B == 1 ? 24 : B == 2 ? 14 : B == 3 ? 10 : 7);
+};
+
+#ifndef SMNN_PIPE_NT
+#define SMNN_PIPE_NT 128
+#endif
+#ifndef SMNN_PIPE_SEP_MAX
+#define SMNN_PIPE_SEP_MAX 1024
+#endif
+
+template <int B>
+struct PSep {
+  static constexpr int LT = B * (B + 1) / 2;
+  static constexpr int D = 0, R = LT, BL = LT + B, AL = LT + B + B * B, RL = 2 * LT + B + B * B;
+  static constexpr int N = 2 * LT + 2 * B + B * B;
+};
+
+struct PipeL {
+  int K;          // chunks (= separators) per instance
+  int NT;         // threads per CTA of the chunk kernels
+  int parts;      // CTAs per instance of the chunk kernels
+  int sepmap;     // separator kernel thread map: 1 = grouped by reduction level, 0 = identity
+  int off_c, off_d, off_s, off_g, off_y, off_h, off_bar;  // shared-memory byte offsets (16-aligned)
+  void* sep1;
+  void* ysep;
+  int* cfail;
+};
+
+// Time range of a chunk-kernel CTA: chunks [c0, c0 + nc), points [ta, tb),
+// steps s staged from slo = max(ta - 1, 0) to shi = min(tb, T - 1).
+struct PRange {
+  int64_t g;
+  int c0, nc, ta, tb, slo, shi;
+  __device__ PRange(const PipeL& L, int T) {
+    g = blockIdx.x / L.parts;
+    const int part = int(blockIdx.x % L.parts);
+    c0 = part * L.NT;
+    nc = min(L.NT, L.K - c0);
+    ta = chunk_begin(c0, T, L.K);
+    tb = chunk_begin(c0 + nc, T, L.K);
+    slo = max(ta - 1, 0);
+    shi = min(tb, T - 1);
+  }
+};
+
+// ============================================================== P1 ========
+template <int B, class Tio, class S, bool BWD, int CM>
+__global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p1_kernel(Args<Tio> a, PipeL L) {
+  using Q = PSep<B>;
+  unsigned char* sm = smnn_dyn_smem;
+  Tio* smT = reinterpret_cast<Tio*>(sm);
+  const int T = a.T, K = L.K, tid = threadIdx.x;
+  const PRange R(L, T);
+  const int64_t g = R.g;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.off_bar);
+  const Wts<S> w{opaque(splat<S>(a.wg2)), opaque(splat<S>(a.wi2)), opaque(splat<S>(a.ws2))};
+  const int64_t tb = g * int64_t(T) * B, t1b = g * int64_t(T), tsb = g * int64_t(T - 1);
+  const Span<Tio> pc(a.coeffs + tb + R.ta * B, (R.tb - R.ta) * B);
+  const Span<Tio> pd(a.rhs + t1b + R.ta, BWD ? 0 : R.tb - R.ta);
+  const Span<Tio> ps(a.steps + tsb + R.slo, R.shi - R.slo);
+  const Span<Tio> pg(BWD ? a.grad_y + tb + R.ta * B : a.coeffs, BWD ? (R.tb - R.ta) * B : 0);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes);
+    bulk_g2s(sm + L.off_c, pc.lo, pc.bytes, bar);
+    if (pd.bytes) bulk_g2s(sm + L.off_d, pd.lo, pd.bytes, bar);
+    if (ps.bytes) bulk_g2s(sm + L.off_s, ps.lo, ps.bytes, bar);
+    if (pg.bytes) bulk_g2s(sm + L.off_g, pg.lo, pg.bytes, bar);
+  }
+  constexpr int E = int(sizeof(Tio));
+  const int k = R.c0 + tid;
+  const bool act = tid < R.nc;
+  const int f = act ? chunk_begin(k, T, K) : R.ta;
+  const int sig = act ? chunk_begin(k + 1, T, K) - 1 : R.ta + 1;
+  const int nint = sig - f;
+  const Tio* cS = smT + opaque(L.off_c / E + pc.pre + (f - R.ta) * B);
+  const Tio* dS = smT + opaque(L.off_d / E + pd.pre + (f - R.ta));
+  const Tio* sS = smT + opaque(L.off_s / E + ps.pre + (f - R.slo));  // sS[-1] = s_{f-1}
+  const Tio* gS = smT + opaque(L.off_g / E + pg.pre + (f - R.ta) * B);
+  const Tio* u = a.iv + g * a.n_iv;
+  __syncthreads();  // barrier initialised
+  mbar_wait(bar, 0);
+
+  S Dsep[B][B], Rsep[B], Arl[B][B], All[B][B], rl[B];
+  bool bad = false;
+  if (act) {
+  S ap[2 * B - 1];
+  if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
+  S Lc[B][B], wv[B], X[B][B];
+  zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
+  S sg = splat<S>(1.0);
+#pragma unroll
+  for (int i = 0; i < CM - 1; ++i) {
+    if (i < nint) {
+      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
+      spow<B, S>(S(sS[i]), w.s2, an);
+      lassemble<B, S>(c, w.g2, ap, an, M, wc);
+      if (BWD) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
+      } else {
+        const S d = S(dS[i]);
+#pragma unroll
+        for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
+      }
+      if (i == 0 && k == 0) {  // initial-value rows at t = 0
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+          if (r < a.n_iv) {
+            if (!BWD) rhs[r] = fma_(w.i2, S(u[r]), rhs[r]);
+            M[r][r] = add_(M[r][r], w.i2);
+          }
+      }
+      if (i == 0) {
+        lchol<B, S>(M, Lc);
+        llsolve<B, S>(Lc, rhs, wv);
+        S NL[B][B];  // spike X_f = L_f^{-1} N_{f-1} (zero for k = 0: ap = 0)
+        lN<B, S>(ap, NL);
+        lleft<B, S>(Lc, NL, X);
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+#pragma unroll
+          for (int q = 0; q <= r; ++q) {
+            S acc = mul_(X[0][r], X[0][q]);
+#pragma unroll
+            for (int m = 1; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
+            All[r][q] = acc;
+          }
+          S acc = mul_(X[0][r], wv[0]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
+          rl[r] = acc;
+        }
+      } else {
+        S Pm[B][B];
+        lPfromN<B, S>(ap, Lc, Pm);  // P_{j-1} = N_{j-1} L_{j-1}^{-T}
+        lcouple<B, S>(Pm, wv, M, rhs);
+        lchol<B, S>(M, Lc);
+        llsolve<B, S>(Lc, rhs, wv);
+        S Y[B][B];  // spike X_j = -L_j^{-1} P_{j-1} X_{j-1}, carried with sign sg
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            S acc = mul_(Pm[r][0], X[0][q]);
+#pragma unroll
+            for (int m = 1; m < B; ++m) acc = fma_(Pm[r][m], X[m][q], acc);
+            Y[r][q] = acc;
+          }
+        lleft<B, S>(Lc, Y, X);
+        sg = neg_(sg);
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+#pragma unroll
+          for (int q = 0; q <= r; ++q) {
+            S acc = All[r][q];
+#pragma unroll
+            for (int m = 0; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
+            All[r][q] = acc;
+          }
+          S acc = mul_(X[0][r], wv[0]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
+          rl[r] = fma_(sg, acc, rl[r]);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+    }
+  }
+  // one pivot check per chunk: a breakdown leaves a non-finite last factor
+  bad = bad_(splat<S>(1.0) / Lc[B - 1][B - 1]) != 0;
+  {  // Schur complement of the interior onto (sigma_{k-1}, sigma_k); ap = a(s_l)
+    S Pl[B][B];
+    lPfromN<B, S>(ap, Lc, Pl);
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        S a2 = mul_(Pl[r][0], X[0][q]);
+#pragma unroll
+        for (int m = 1; m < B; ++m) a2 = fma_(Pl[r][m], X[m][q], a2);
+        Arl[r][q] = mul_(neg_(sg), a2);
+      }
+    S c[B], an[2 * B - 1], wc[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) c[r] = S(cS[nint * B + r]);
+    if (k + 1 < K) spow<B, S>(S(sS[nint]), w.s2, an); else zero<2 * B - 1, S>(an);
+    lassemble<B, S>(c, w.g2, ap, an, Dsep, wc);
+    if (BWD) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) Rsep[r] = S(gS[nint * B + r]);
+    } else {
+      const S d = S(dS[nint]);
+#pragma unroll
+      for (int r = 0; r < B; ++r) Rsep[r] = mul_(wc[r], d);
+    }
+    lcouple<B, S>(Pl, wv, Dsep, Rsep);
+  }
+  }  // act
+  // A_ll = -sum X^T X, r_l = -sum X^T w belong to separator k - 1: hand them to
+  // the left neighbour through shared memory (the staged inputs are still in
+  // use, so a region of its own); a CTA's first chunk writes them to the
+  // workspace for the previous CTA's last separator.
+  S* ho = reinterpret_cast<S*>(sm + L.off_h);
+  constexpr int HN = Q::LT + B;
+  if (act) {
+    int e = 0;
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int q = 0; q <= r; ++q) ho[(e++) * SMNN_PIPE_NT + tid] = neg_(All[r][q]);
+#pragma unroll
+    for (int r = 0; r < B; ++r) ho[(Q::LT + r) * SMNN_PIPE_NT + tid] = neg_(rl[r]);
+  }
+  __syncthreads();
+  if (!act) return;
+  if (tid + 1 < R.nc) {
+    int e = 0;
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int q = 0; q <= r; ++q) Dsep[r][q] = add_(Dsep[r][q], ho[(e++) * SMNN_PIPE_NT + tid + 1]);
+#pragma unroll
+    for (int r = 0; r < B; ++r) Rsep[r] = add_(Rsep[r], ho[(Q::LT + r) * SMNN_PIPE_NT + tid + 1]);
+  }
+  (void)HN;
+  // write the separator blocks (field-major: coalesced across the warp)
+  S* o = reinterpret_cast<S*>(L.sep1) + g * int64_t(Q::N) * K + k;
+  int e = 0;
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int q = 0; q <= r; ++q) o[int64_t(Q::D + e++) * K] = Dsep[r][q];
+#pragma unroll
+  for (int r = 0; r < B; ++r) o[int64_t(Q::R + r) * K] = Rsep[r];
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int q = 0; q < B; ++q) o[int64_t(Q::BL + r * B + q) * K] = Arl[r][q];
+  if (tid == 0 && k > 0) {  // the previous CTA's last separator adds these (psep_nb)
+    e = 0;
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int q = 0; q <= r; ++q) o[int64_t(Q::AL + e++) * K] = neg_(All[r][q]);
+#pragma unroll
+    for (int r = 0; r < B; ++r) o[int64_t(Q::RL + r) * K] = neg_(rl[r]);
+  }
+  L.cfail[g * K + k] = bad ? f + 1 : INT_MAX;  // 1 + first point of the chunk
+}
+
+// ============================================================== SEP =======
+template <int B, class S>
+__global__ void __launch_bounds__(SMNN_PIPE_SEP_MAX, 1) pipe_sep_kernel(PipeL L, int T, int32_t* info) {
+  using Q = PSep<B>;
+  using BR = BRec<B>;
+  unsigned char* sm = smnn_dyn_smem;
+  // threads ordered by the level at which their separator is eliminated
+  // (rf_chunk_of_thread): each reduction level runs on as few warps as possible
+  const int K = L.K, k = L.sepmap ? rf_chunk_of_thread(int(threadIdx.x), K) : int(threadIdx.x);
+  const int64_t g = blockIdx.x;
+  S* rec = reinterpret_cast<S*>(sm);
+  int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * K);
+  int* sfail = stime + K;
+  if (k == 0) sfail[0] = INT_MAX;
+  stime[k] = chunk_begin(k + 1, T, K) - 1;
+  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(Q::N) * K;
+  S D[B][B], Bl[B][B], Cr[B][B], r[B];
+  int e = 0;
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int q = 0; q <= i; ++q) D[i][q] = in[int64_t(Q::D + e++) * K + k];
+#pragma unroll
+  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + k];
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + k];
+  if (k + 1 < K) {  // the coupling to sigma_{k+1} (and A_ll, r_l across a P1 CTA boundary)
+    if ((k + 1) % L.NT == 0) {
+      e = 0;
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], in[int64_t(Q::AL + e++) * K + k + 1]);
+#pragma unroll
+      for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + k + 1]);
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+      for (int q = 0; q < B; ++q) Cr[i][q] = in[int64_t(Q::BL + q * B + i) * K + k + 1];
+  } else {
+    zero<B, S>(Cr);
+  }
+  const int cf = L.cfail[g * K + k];
+  __syncthreads();
+  if (cf != INT_MAX) atomicMin(sfail, cf);
+  rbcr2<B, S>(rec, K, k, stime, sfail, D, Bl, Cr, r);
+  S* y = reinterpret_cast<S*>(L.ysep) + g * int64_t(B) * K + k;
+#pragma unroll
+  for (int i = 0; i < B; ++i) y[int64_t(i) * K] = rec[k * BR::N + BR::Y + i];
+  if (k == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
+}
+
+
+// ========================================================== SEP, large K ===
+// The separator system is itself block tridiagonal with explicit blocks
+// (D_j = D_own_j + A_ll,j+1, r_j = R_own_j + r_l,j+1, coupling (j, j-1) = A_rl,j).
+// For large K the partition method is applied to it once more: thread t owns
+// m consecutive separators j0 = t m .. j0 + m - 1, block-Cholesky-eliminates
+// the first m - 1 (with the spike towards super-separator t - 1, factors kept
+// in registers), the K/m super-separators j0 + m - 1 are solved by rbcr2, and
+// the owned separators are recovered by forward + back substitution.
+template <int B, class S>
+__device__ __forceinline__ void psep_ld(const S* in, int K, int NT, int j, S (&D)[B][B], S (&r)[B], S (&Bl)[B][B]) {
+  using Q = PSep<B>;
+  int e = 0;
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int q = 0; q <= i; ++q) D[i][q] = in[int64_t(Q::D + e++) * K + j];
+#pragma unroll
+  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + j];
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
+  if (j + 1 < K && (j + 1) % NT == 0) {
+    e = 0;
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+      for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], in[int64_t(Q::AL + e++) * K + j + 1]);
+#pragma unroll
+    for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + j + 1]);
+  }
+}
+
+template <int B, class S>
+__device__ __forceinline__ void psep_ld_rb(const S* in, int K, int NT, int j, S (&r)[B], S (&Bl)[B][B]) {
+  using Q = PSep<B>;
+#pragma unroll
+  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + j];
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
+  if (j + 1 < K && (j + 1) % NT == 0) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + j + 1]);
+  }
+}
+template <int B, class S>
+__device__ __forceinline__ void psep_ld_b(const S* in, int K, int j, S (&Bl)[B][B]) {
+  using Q = PSep<B>;
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
+}
+
+template <int B, class S, int MS>
+__global__ void __launch_bounds__(256, 3) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
+  using BR = BRec<B>;
+  unsigned char* sm = smnn_dyn_smem;
+  const int K = L.K, nt = blockDim.x, t = threadIdx.x;
+  const int m = K / nt;  // separators per thread (host: K = m * nt, m <= MS)
+  const int64_t g = blockIdx.x;
+  S* rec = reinterpret_cast<S*>(sm);
+  int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * nt);
+  int* sfail = stime + nt;
+  const int j0 = t * m, js = j0 + m - 1;
+  if (t == 0) sfail[0] = INT_MAX;
+  stime[t] = chunk_begin(js + 1, T, K) - 1;
+  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B>::N) * K;
+  int cf = INT_MAX;
+  for (int j = j0; j <= js; ++j) cf = min(cf, L.cfail[g * K + j]);
+  // ---- eliminate the owned interior separators j0 .. js-1 (spike towards t-1)
+  S Lr[MS - 1][B][B];
+  S Lc[B][B], wv[B], X[B][B], All[B][B], rl[B], Pl[B][B];
+  zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
+  S sg = splat<S>(1.0);
+#pragma unroll
+  for (int i = 0; i < MS - 1; ++i) {
+    S D[B][B], r[B], Bl[B][B];
+    psep_ld<B, S>(in, K, L.NT, j0 + min(i, m - 2), D, r, Bl);  // unconditional: lets the loads run ahead
+    if (i < m - 1) {
+      if (i == 0) {  // Bl couples to super-separator t - 1 (zero for t = 0)
+        lchol<B, S>(D, Lc);
+        llsolve<B, S>(Lc, r, wv);
+        lleft<B, S>(Lc, Bl, X);
+#pragma unroll
+        for (int a = 0; a < B; ++a) {
+#pragma unroll
+          for (int q = 0; q <= a; ++q) {
+            S acc = mul_(X[0][a], X[0][q]);
+#pragma unroll
+            for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
+            All[a][q] = acc;
+          }
+          S acc = mul_(X[0][a], wv[0]);
+#pragma unroll
+          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
+          rl[a] = acc;
+        }
+      } else {
+        S Pm[B][B];  // P = Bl_j L_{j-1}^{-T}
+#pragma unroll
+        for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pm[a]);
+        lcouple<B, S>(Pm, wv, D, r);
+        lchol<B, S>(D, Lc);
+        llsolve<B, S>(Lc, r, wv);
+        S Y[B][B];
+#pragma unroll
+        for (int a = 0; a < B; ++a)
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            S acc = mul_(Pm[a][0], X[0][q]);
+#pragma unroll
+            for (int mm = 1; mm < B; ++mm) acc = fma_(Pm[a][mm], X[mm][q], acc);
+            Y[a][q] = acc;
+          }
+        lleft<B, S>(Lc, Y, X);
+        sg = neg_(sg);
+#pragma unroll
+        for (int a = 0; a < B; ++a) {
+#pragma unroll
+          for (int q = 0; q <= a; ++q) {
+            S acc = All[a][q];
+#pragma unroll
+            for (int mm = 0; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
+            All[a][q] = acc;
+          }
+          S acc = mul_(X[0][a], wv[0]);
+#pragma unroll
+          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
+          rl[a] = fma_(sg, acc, rl[a]);
+        }
+      }
+      rcopyL<B, S>(Lc, Lr[i]);
+    }
+  }
+  // ---- the super-separator js: own block minus the interior's Schur terms
+  S Ds[B][B], Rs[B], Bs[B][B];
+  {
+    S Bl[B][B];
+    psep_ld<B, S>(in, K, L.NT, js, Ds, Rs, Bl);
+    if (m > 1) {
+#pragma unroll
+      for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pl[a]);
+      lcouple<B, S>(Pl, wv, Ds, Rs);
+#pragma unroll
+      for (int a = 0; a < B; ++a)
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          S acc = mul_(Pl[a][0], X[0][q]);
+#pragma unroll
+          for (int mm = 1; mm < B; ++mm) acc = fma_(Pl[a][mm], X[mm][q], acc);
+          Bs[a][q] = mul_(neg_(sg), acc);
+        }
+    } else {
+#pragma unroll
+      for (int a = 0; a < B; ++a)
+#pragma unroll
+        for (int q = 0; q < B; ++q) Bs[a][q] = Bl[a][q];
+    }
+  }
+  if (m > 1 && bad_(splat<S>(1.0) / Lc[B - 1][B - 1])) cf = min(cf, 1 + (chunk_begin(j0 + 1, T, K) - 1));
+  // hand-over (A_ll, r_l, coupling) to super-separator t - 1
+  S* pk = rec + t * BR::N;
+#pragma unroll
+  for (int a = 0; a < B; ++a) {
+    rl[a] = neg_(rl[a]);
+#pragma unroll
+    for (int q = 0; q <= a; ++q) All[a][q] = neg_(All[a][q]);
+  }
+  rst_tri<B, S>(pk + BR::HA, All);
+  rst_full<B, S>(pk + BR::HB, Bs);
+  rst_v<B, S>(pk + BR::HR, rl);
+  __syncthreads();
+  S Cs[B][B];
+  if (t + 1 < nt) {
+    S Al[B][B], An[B][B], rr[B];
+    const S* pn = rec + (t + 1) * BR::N;
+    rld_tri<B, S>(pn + BR::HA, Al);
+    rld_full<B, S>(pn + BR::HB, An);
+    rld_v<B, S>(pn + BR::HR, rr);
+#pragma unroll
+    for (int a = 0; a < B; ++a) {
+      Rs[a] = add_(Rs[a], rr[a]);
+#pragma unroll
+      for (int q = 0; q <= a; ++q) Ds[a][q] = add_(Ds[a][q], Al[a][q]);
+#pragma unroll
+      for (int q = 0; q < B; ++q) Cs[a][q] = An[q][a];
+    }
+  } else {
+    zero<B, S>(Cs);
+  }
+  if (cf != INT_MAX) atomicMin(sfail, cf);
+  __syncthreads();  // hand-over slots are reused by the reduction
+  rbcr2<B, S>(rec, nt, t, stime, sfail, Ds, Bs, Cs, Rs);
+  S yR[B], yL[B];
+  rld_v<B, S>(rec + t * BR::N + BR::Y, yR);
+  if (t > 0) rld_v<B, S>(rec + (t - 1) * BR::N + BR::Y, yL); else zero<B, S>(yL);
+  // ---- recover the owned separators: forward substitution with y_L, back substitution from y_R
+  S* yo = reinterpret_cast<S*>(L.ysep) + g * int64_t(B) * K;
+#pragma unroll
+  for (int a = 0; a < B; ++a) yo[int64_t(a) * K + js] = yR[a];
+  S Wp[MS - 1][B];
+#pragma unroll
+  for (int i = 0; i < MS - 1; ++i) {
+    S r[B], Bl[B][B];
+    psep_ld_rb<B, S>(in, K, L.NT, j0 + min(i, m - 2), r, Bl);
+    if (i < m - 1) {
+      S tv[B], u[B];
+      if (i == 0) {
+#pragma unroll
+        for (int a = 0; a < B; ++a) tv[a] = yL[a];
+      } else {
+        lltsolve<B, S>(Lr[i - 1], Wp[i - 1], tv);
+      }
+#pragma unroll
+      for (int a = 0; a < B; ++a) {
+        S acc = r[a];
+#pragma unroll
+        for (int q = 0; q < B; ++q) acc = fnma_(Bl[a][q], tv[q], acc);
+        u[a] = acc;
+      }
+      llsolve<B, S>(Lr[i], u, Wp[i]);
+    }
+  }
+  S yn[B];
+#pragma unroll
+  for (int a = 0; a < B; ++a) yn[a] = yR[a];
+#pragma unroll
+  for (int i = MS - 2; i >= 0; --i) {
+    S Bn[B][B];
+    psep_ld_b<B, S>(in, K, j0 + min(i, m - 2) + 1, Bn);  // coupling (j+1, j)
+    if (i < m - 1) {
+      S v[B], u[B], tv[B], yv[B];
+#pragma unroll
+      for (int a = 0; a < B; ++a) {
+        S acc = mul_(Bn[0][a], yn[0]);
+#pragma unroll
+        for (int q = 1; q < B; ++q) acc = fma_(Bn[q][a], yn[q], acc);
+        v[a] = acc;
+      }
+      llsolve<B, S>(Lr[i], v, u);
+#pragma unroll
+      for (int a = 0; a < B; ++a) tv[a] = sub_(Wp[i][a], u[a]);
+      lltsolve<B, S>(Lr[i], tv, yv);
+#pragma unroll
+      for (int a = 0; a < B; ++a) yo[int64_t(a) * K + j0 + i] = yv[a];
+#pragma unroll
+      for (int a = 0; a < B; ++a) yn[a] = yv[a];
+    }
+  }
+  if (t == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
+}
+
+// ============================================================== P2 ========
+template <int B, class Tio, class S, bool BWD, int CM>
+__global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p2_kernel(Args<Tio> a, PipeL L) {
+  unsigned char* sm = smnn_dyn_smem;
+  Tio* smT = reinterpret_cast<Tio*>(sm);
+  const int T = a.T, K = L.K, tid = threadIdx.x;
+  const PRange R(L, T);
+  const int64_t g = R.g;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.off_bar);
+  const Wts<S> w{opaque(splat<S>(a.wg2)), opaque(splat<S>(a.wi2)), opaque(splat<S>(a.ws2))};
+  const int64_t tb = g * int64_t(T) * B, t1b = g * int64_t(T), tsb = g * int64_t(T - 1);
+  const int ylo = R.slo;  // BWD: y_fwd from max(ta - 1, 0)
+  const Span<Tio> pc(a.coeffs + tb + R.ta * B, (R.tb - R.ta) * B);
+  const Span<Tio> pd(a.rhs + t1b + R.ta, R.tb - R.ta);
+  const Span<Tio> ps(a.steps + tsb + R.slo, R.shi - R.slo);
+  const Span<Tio> pg(BWD ? a.grad_y + tb + R.ta * B : a.coeffs, BWD ? (R.tb - R.ta) * B : 0);
+  const Span<Tio> py(BWD ? a.y_in + tb + ylo * B : a.coeffs, BWD ? (R.tb - ylo) * B : 0);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes);
+    bulk_g2s(sm + L.off_c, pc.lo, pc.bytes, bar);
+    bulk_g2s(sm + L.off_d, pd.lo, pd.bytes, bar);
+    if (ps.bytes) bulk_g2s(sm + L.off_s, ps.lo, ps.bytes, bar);
+    if (BWD) {
+      bulk_g2s(sm + L.off_g, pg.lo, pg.bytes, bar);
+      bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
+    }
+  }
+  constexpr int E = int(sizeof(Tio));
+  const int k = R.c0 + tid;
+  const bool act = tid < R.nc;
+  const int f = act ? chunk_begin(k, T, K) : R.ta;
+  const int sig = act ? chunk_begin(k + 1, T, K) - 1 : R.ta + 1;
+  const int nint = sig - f;
+  // element offsets of the staged streams, relative to global time index 0
+  const int oc = L.off_c / E + pc.pre - R.ta * B, od = L.off_d / E + pd.pre - R.ta;
+  const int os = L.off_s / E + ps.pre - R.slo;
+  const int og = BWD ? L.off_g / E + pg.pre - R.ta * B : 0, oy = BWD ? L.off_y / E + py.pre - ylo * B : 0;
+  Grp<Tio, 1> x;
+  x.T = T; x.n_iv = a.n_iv; x.nv = 1;
+  x.c.o[0] = oc; x.d.o[0] = od; x.s.o[0] = os; x.gy.o[0] = og; x.yin.o[0] = oy;
+  x.yout.o[0] = oc; x.gc.o[0] = oc; x.gd.o[0] = od; x.gs.o[0] = os;
+  x.u[0] = a.iv + g * a.n_iv;
+  x.gu[0] = (BWD && a.g_iv) ? a.g_iv + g * a.n_iv : nullptr;
+  x.c.on = x.d.on = x.s.on = true;
+  x.gy.on = x.yin.on = BWD;
+  x.yout.on = !BWD;
+  x.gc.on = BWD && a.g_coeffs;
+  x.gd.on = BWD && a.g_rhs;
+  x.gs.on = BWD && a.g_steps;
+  x.gu_on = BWD && a.g_iv;
+  const Tio* cS = smT + opaque(oc + f * B);
+  const Tio* dS = smT + opaque(od + f);
+  const Tio* sS = smT + opaque(os + f);
+  const Tio* gS = smT + opaque(og + f * B);
+  S yL[B], yR[B];
+  if (act) {
+    const S* ys = reinterpret_cast<const S*>(L.ysep) + g * int64_t(B) * K + k;
+#pragma unroll
+    for (int i = 0; i < B; ++i) yR[i] = ys[int64_t(i) * K];
+    if (k > 0) {
+#pragma unroll
+      for (int i = 0; i < B; ++i) yL[i] = ys[int64_t(i) * K - 1];
+    } else {
+      zero<B, S>(yL);
+    }
+  }
+  __syncthreads();  // barrier initialised
+  mbar_wait(bar, 0);
+
+  if (act) {
+    // forward sweep: re-factor the interior and forward-substitute with y_L known
+    S Lr[CM - 1][B][B], Wp[CM - 1][B];
+    {
+      S ap[2 * B - 1];
+      if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
+#pragma unroll
+      for (int i = 0; i < CM - 1; ++i) {
+        if (i < nint) {
+          S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
+#pragma unroll
+          for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
+          spow<B, S>(S(sS[i]), w.s2, an);
+          lassemble<B, S>(c, w.g2, ap, an, M, wc);
+          if (BWD) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
+          } else {
+            const S d = S(dS[i]);
+#pragma unroll
+            for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
+          }
+          if (i == 0) {
+            if (k == 0) {
+#pragma unroll
+              for (int r = 0; r < B; ++r)
+                if (r < a.n_iv) {
+                  if (!BWD) rhs[r] = fma_(w.i2, S(x.u[0][r]), rhs[r]);
+                  M[r][r] = add_(M[r][r], w.i2);
+                }
+            }
+            S Nt[B];  // rhs -= N_{f-1} y_L
+            rNv<B, S>(ap, yL, Nt);
+#pragma unroll
+            for (int r = 0; r < B; ++r) rhs[r] = sub_(rhs[r], Nt[r]);
+          } else {
+            S Pm[B][B];
+            lPfromN<B, S>(ap, Lr[i - 1], Pm);
+            lcouple<B, S>(Pm, Wp[i - 1], M, rhs);
+          }
+          lchol<B, S>(M, Lr[i]);
+          llsolve<B, S>(Lr[i], rhs, Wp[i]);
+#pragma unroll
+          for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+        }
+      }
+    }
+    // back substitution from y_{sigma_k} (as the RF kernel's pass 2)
+    S yn[B], yfn[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) yn[r] = yR[r];
+    zero<B, S>(yfn);
+    if (!BWD) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, sig * B + r, yR[r]);
+    } else {
+      ldlv<B, S, Tio, 1, true>(x.yin, sig * B, yfn);
+      lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR, yfn);
+    }
+#pragma unroll
+    for (int i = CM - 2; i >= 0; --i) {
+      if (i < nint) {
+        const int j = f + i;
+        S an[2 * B - 1], v[B], uu[B], t[B], yv[B];
+        spow<B, S>(S(sS[i]), w.s2, an);
+        rNtv<B, S>(an, yn, v);
+        llsolve<B, S>(Lr[i], v, uu);
+#pragma unroll
+        for (int r = 0; r < B; ++r) t[r] = sub_(Wp[i][r], uu[r]);
+        lltsolve<B, S>(Lr[i], t, yv);
+        if (!BWD) {
+#pragma unroll
+          for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[r]);
+        } else {
+          S yf[B];
+          ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
+          lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv, yf);
+          if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv, yf, yn, yfn));
+#pragma unroll
+          for (int r = 0; r < B; ++r) yfn[r] = yf[r];
+        }
+#pragma unroll
+        for (int r = 0; r < B; ++r) yn[r] = yv[r];
+      }
+    }
+    if (BWD && k > 0 && x.gs.on) {  // interval (sigma_{k-1}, f)
+      S yfm[B], am[2 * B - 1];
+      ldlv<B, S, Tio, 1, true>(x.yin, (f - 1) * B, yfm);
+      spow<B, S>(S(sS[-1]), w.s2, am);
+      stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL, yfm, yn, yfn));
+    }
+  }
+  // ---- outputs: TMA bulk store of the aligned body, plain stores at the ends
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const int nt = blockDim.x;
+  if (!BWD) {
+    rf_store_out(a.y_out + tb + R.ta * B, smT + oc + R.ta * B, (R.tb - R.ta) * B, tid, nt);
+  } else {
+    if (a.g_coeffs) rf_store_out(a.g_coeffs + tb + R.ta * B, smT + oc + R.ta * B, (R.tb - R.ta) * B, tid, nt);
+    if (a.g_rhs) rf_store_out(a.g_rhs + t1b + R.ta, smT + od + R.ta, R.tb - R.ta, tid, nt);
+    if (a.g_steps && R.tb - 1 > R.slo)  // this CTA owns intervals [slo, tb - 1)
+      rf_store_out(a.g_steps + tsb + R.slo, smT + os + R.slo, R.tb - 1 - R.slo, tid, nt);
+  }
+  if (tid == 0) {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+}  // namespace smnn

@@ -21,21 +21,6 @@ namespace {
 
 size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
-int sms() {
-  static int v = 0;
-  if (v == 0) {
-    int dev = 0, n = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    v = n;
-  }
-  return v;
-}
-
-bool rf_disabled() {
-  const char* e = std::getenv("SMNN_KERNEL");
-  return e && std::string(e) != "rf" && std::string(e) != "auto";
-}
-
 // Chunks (= threads) per instance: the fewest multiple-of-32 count whose
 // chunks hold at most CM points, with every chunk >= 2 points (an interior).
 int rf_threads(const smnn_problem* p, int CM) {
@@ -125,7 +110,6 @@ int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std
 
 template <class Tio, class Tc>
 int rf_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err) {
-  if (rf_disabled()) return 0;
   return bwd ? launch_order<Tio, Tc, true>(p, a, st, err) : launch_order<Tio, Tc, false>(p, a, st, err);
 }
 

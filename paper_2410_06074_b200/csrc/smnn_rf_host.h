@@ -19,4 +19,11 @@ struct Args;
 template <class Tio, class Tc>
 int rf_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err);
 
+// Three-kernel pipeline (smnn_pipe.cu): same contract as rf_launch; its
+// workspace (separator blocks, separator solution, chunk failure flags) is
+// carved from Args::ckpt, which must hold pipe_workspace_bytes(p).
+template <class Tio, class Tc>
+int pipe_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err);
+size_t pipe_workspace_bytes(const smnn_problem* p);
+
 }  // namespace smnn
