@@ -253,7 +253,12 @@ def main():
     units = wl.n_inst * wl.T * world
     value = units / (ms_per_step / 1e3)
 
-    # roofline of the dominant kernel (algorithmic bytes / measured launch time)
+    paths = {d: smnn.kernel_path(wl.n_inst, wl.T, wl.order, wl.n_iv, tdtype, compute, bwd=(d == "bwd"))
+             for d in ("fwd", "bwd")}
+    from paper_2410_06074_b200 import _abi
+    launches = {d: _abi.PATH_LAUNCHES[{"rf": 1, "pipe": 2, "checkpoint": 3}[v]] for d, v in paths.items()}
+    # roofline of the dominant launch (algorithmic bytes / measured launch time); for the
+    # pipeline path the "launch" is the call's three back-to-back kernels
     fb, bb = algorithmic_bytes(b, es)
     f_avg, b_avg = float(np.mean(fwd_ms)), float(np.mean(bwd_ms))
     inst_steps = wl.n_inst * wl.T
@@ -261,6 +266,10 @@ def main():
     kern = "smnn_solve_bwd" if b_avg >= f_avg else "smnn_factor_solve_fwd"
     kbytes = inst_steps * (bb if b_avg >= f_avg else fb)
     kms = max(b_avg, f_avg)
+    kdir = "bwd" if b_avg >= f_avg else "fwd"
+    kernel_label = kern + {"rf": " = rf_kernel (one launch)",
+                           "pipe": " = pipe_p1 + pipe_sep + pipe_p2 (three launches)",
+                           "checkpoint": " = resident/fused checkpoint kernel (one launch)"}[paths[kdir]]
     achieved = kbytes / (kms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -314,12 +323,14 @@ def main():
                        store == "f64" else "f32", "l2": "flushed between timed steps (256 MiB write)",
                        "parallelism": f"dp{world} (instances sharded, no data-path collective)",
                        "threads_per_inst": tpi or "auto"},
-            "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+            "roofline": {"bound": "hbm", "kernel": kernel_label,
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": kbytes, "launch_ms": kms,
                          "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
             "kernels_ms": {"smnn_factor_solve_fwd": f_avg, "smnn_solve_bwd": b_avg},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": (launches["fwd"] + launches["bwd"]) * args.steps,
+            "kernel_path": paths,
             "clocks": clk.result(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -82,6 +82,20 @@ typedef struct smnn_problem {
 const char* smnn_version(void);
 const char* smnn_last_error(void);
 
+/* Which kernels smnn_factor_solve_fwd (bwd = 0) / smnn_solve_bwd (bwd = 1)
+ * run for `p` on this build (environment SMNN_KERNEL = auto | rf | pipe |
+ * resident | stream overrides the automatic choice, for experiments):
+ *   SMNN_PATH_RF          one launch: resident register-factor kernel (one CTA
+ *                         per instance, whole instance in shared memory)
+ *   SMNN_PATH_PIPE        three launches: chunk pass 1, separator reduction,
+ *                         chunk pass 2 (long horizons; needs the workspace)
+ *   SMNN_PATH_CHECKPOINT  one launch: checkpointing resident / streaming kernel
+ * Returns a negative SMNN_ERR_* code on an invalid `p`. */
+#define SMNN_PATH_RF 1
+#define SMNN_PATH_PIPE 2
+#define SMNN_PATH_CHECKPOINT 3
+int smnn_kernel_path(const smnn_problem* p, int bwd);
+
 /* Bytes of device workspace the fused kernels need for `p` on the current
  * device (checkpoint scratch of the time-parallel solver, one slot per
  * resident CTA).  Pass at least this much to smnn_factor_solve_fwd /

@@ -15,8 +15,11 @@ ERRORS = {-1: "SMNN_ERR_ARG", -2: "SMNN_ERR_CUDA", -3: "SMNN_ERR_UNSUPPORTED", -
 EXPORTED = [
     "smnn_version", "smnn_last_error", "smnn_workspace_bytes", "smnn_assemble",
     "smnn_factor_solve_fwd", "smnn_solve_bwd", "smnn_factor", "smnn_substitute",
-    "smnn_plan_create", "smnn_plan_destroy", "smnn_plan_fwd_bwd_host",
+    "smnn_plan_create", "smnn_plan_destroy", "smnn_plan_fwd_bwd_host", "smnn_kernel_path",
 ]
+SMNN_PATH_RF, SMNN_PATH_PIPE, SMNN_PATH_CHECKPOINT = 1, 2, 3
+PATH_NAMES = {1: "rf", 2: "pipe", 3: "checkpoint"}
+PATH_LAUNCHES = {1: 1, 2: 3, 3: 1}
 
 
 class smnn_problem(ctypes.Structure):
@@ -57,6 +60,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     L.smnn_version.argtypes = []
     L.smnn_last_error.restype = ctypes.c_char_p
     L.smnn_last_error.argtypes = []
+    L.smnn_kernel_path.restype = ctypes.c_int
+    L.smnn_kernel_path.argtypes = [PP, ctypes.c_int]
     L.smnn_workspace_bytes.restype = ctypes.c_size_t
     L.smnn_workspace_bytes.argtypes = [PP]
     L.smnn_assemble.restype = ctypes.c_int

@@ -589,25 +589,31 @@ int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
   return check_cuda(cudaGetLastError(), "fused kernel launch");
 }
 
+// Kernel path of the fused calls (SMNN_PATH_*), environment SMNN_KERNEL =
+// auto (default) | rf | pipe | resident | stream.  Measured on B200: the
+// resident RF kernel wins while one CTA holds the instance (T <~ 4k); the
+// pipeline beyond it (T = 1e4: 3x the streaming kernel), except fp64
+// arithmetic at order 3 (register spills); then the checkpointing kernels.
+int kernel_path(const smnn_problem* p, bool bwd) {
+  const char* env = std::getenv("SMNN_KERNEL");
+  const std::string mode = env ? env : "auto";
+  if ((mode == "auto" || mode == "rf") && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
+  const bool c64 = p->dtype != SMNN_F32;
+  if ((mode == "pipe" || (mode == "auto" && !(c64 && p->order >= 3))) && smnn::pipe_eligible(p, bwd))
+    return SMNN_PATH_PIPE;
+  return SMNN_PATH_CHECKPOINT;
+}
+
 template <class Tio, class Tc, bool BWD>
 int dispatch_fused(const smnn_problem* p, const smnn::Args<Tio>& a, cudaStream_t st) {
-  {  // SMNN_KERNEL = auto (default) | pipe | rf | resident | stream
-    const char* env = std::getenv("SMNN_KERNEL");
-    const std::string mode = env ? env : "auto";
+  {
+    const int path = kernel_path(p, BWD);
     std::string err;
-    // measured on B200: the resident RF kernel wins while one CTA holds the
-    // instance (T <~ 4k); the pipeline beyond (T = 1e4: 2.1x the streaming
-    // kernel), except fp64 arithmetic at order 3 (register spills)
-    if (mode == "auto" || mode == "rf") {  // register-factor resident kernel (smnn_rf.cuh)
-      const int r = smnn::rf_launch<Tio, Tc>(p, a, BWD, st, err);
-      if (r < 0) { g_err = err; return r; }
-      if (r == 1) return SMNN_OK;
-    }
-    if (mode == "pipe" || (mode == "auto" && !(sizeof(Tc) == 8 && p->order >= 3))) {  // smnn_pipe.cuh
-      const int r = smnn::pipe_launch<Tio, Tc>(p, a, BWD, st, err);
-      if (r < 0) { g_err = err; return r; }
-      if (r == 1) return SMNN_OK;
-    }
+    int r = 0;
+    if (path == SMNN_PATH_RF) r = smnn::rf_launch<Tio, Tc>(p, a, BWD, st, err);
+    if (path == SMNN_PATH_PIPE) r = smnn::pipe_launch<Tio, Tc>(p, a, BWD, st, err);
+    if (r < 0) { g_err = err; return r; }
+    if (r == 1) return SMNN_OK;
   }
   switch (p->order) {
     case 0: return launch_fused<1, Tio, Tc, BWD>(p, a, st);
@@ -686,6 +692,12 @@ extern "C" {
 
 const char* smnn_version(void) { return "smnn-b200 0.1 (sm_100a)"; }
 const char* smnn_last_error(void) { return g_err.c_str(); }
+
+int smnn_kernel_path(const smnn_problem* p, int bwd) {
+  int e;
+  if ((e = validate(p))) return e;
+  return kernel_path(p, bwd != 0);
+}
 
 size_t smnn_workspace_bytes(const smnn_problem* p) {
   if (validate(p) != SMNN_OK) return 0;

@@ -20,7 +20,8 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 struct PipePlan {
   bool ok = false;
   int K = 0, NT = 0, parts = 0, CM = 0;
-  bool sep2 = false;  // separator kernel: pipe_sep2_kernel (128 threads, K/128 separators each)
+  bool sep2 = false;  // separator kernel: pipe_sep2_kernel (K/m2 threads, m2 separators each)
+  int m2 = 4;
   size_t smem_p1 = 0, smem_p2 = 0, smem_sep = 0;
   size_t ws_sep1 = 0, ws_ysep = 0, ws_fail = 0;
   PipeL L1{}, L2{};
@@ -38,6 +39,11 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
   if (K > 256) K = std::min((K + 127) / 128 * 128, T / 2);  // large K: 4 separators per thread (sep2)
   if (K < 1 || K > SMNN_PIPE_SEP_MAX || (T + K - 1) / K > CM) return q;
   q.sep2 = K > 256 && K % 128 == 0;
+  {
+    const char* e = std::getenv("SMNN_PIPE_M");
+    q.m2 = e ? std::max(2, std::min(8, std::atoi(e))) : 4;
+    while (q.m2 > 2 && (K % (32 * q.m2) != 0 || K / q.m2 > 256)) q.m2 = (q.m2 == 8) ? 4 : q.m2 - 1;
+  }
   const size_t ls = sizeof(S);
   q.K = K;
   q.CM = CM;
@@ -58,7 +64,7 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
   };
   q.smem_p1 = layout(q.L1, false);
   q.smem_p2 = layout(q.L2, true);
-  q.smem_sep = size_t(BRec<B>::N) * (q.sep2 ? K / 4 : K) * ls + size_t(2 * K + 4) * 4;
+  q.smem_sep = size_t(BRec<B>::N) * (q.sep2 ? K / q.m2 : K) * ls + size_t(2 * K + 4) * 4;
   if (q.smem_p1 > 200 * 1024 || q.smem_p2 > 200 * 1024 || q.smem_sep > 220 * 1024) return q;
   q.ws_sep1 = al256(size_t(p->n_inst) * PSep<B>::N * K * ls);
   q.ws_ysep = al256(size_t(p->n_inst) * B * K * ls);
@@ -68,7 +74,7 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     L->NT = q.NT;
     L->parts = q.parts;
     const char* e = std::getenv("SMNN_PIPE_SEPMAP");
-    L->sepmap = e ? std::atoi(e) : 1;
+    L->sepmap = e ? std::atoi(e) : 0;
   }
   q.ok = true;
   return q;
@@ -114,14 +120,14 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   const unsigned grid_c = unsigned(p->n_inst * q.parts);
   auto k1 = pipe_p1_kernel<B, Tio, S, BWD, CM>;
   auto k2 = pipe_sep_kernel<B, S>;
-  auto k2b = pipe_sep2_kernel<B, S, 4>;
+  auto k2b = q.m2 > 4 ? pipe_sep2_kernel<B, S, 8> : pipe_sep2_kernel<B, S, 4>;
   auto k3 = pipe_p2_kernel<B, Tio, S, BWD, CM>;
   set_smem(k1, q.smem_p1);
   set_smem(k3, q.smem_p2);
   k1<<<grid_c, q.NT, q.smem_p1, st>>>(a, q.L1);
   if (q.sep2) {
     set_smem(k2b, q.smem_sep);
-    k2b<<<unsigned(p->n_inst), q.K / 4, q.smem_sep, st>>>(q.L1, p->T, a.info);
+    k2b<<<unsigned(p->n_inst), q.K / q.m2, q.smem_sep, st>>>(q.L1, p->T, a.info);
   } else {
     set_smem(k2, q.smem_sep);
     k2<<<unsigned(p->n_inst), q.K, q.smem_sep, st>>>(q.L1, p->T, a.info);
@@ -146,6 +152,8 @@ int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std
 }
 
 }  // namespace
+
+bool pipe_eligible(const smnn_problem* p, bool bwd) { return plan_of(p, bwd).ok; }
 
 size_t pipe_workspace_bytes(const smnn_problem* p) {
   const PipePlan f = plan_of(p, false), b = plan_of(p, true);

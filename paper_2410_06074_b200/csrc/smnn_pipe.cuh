@@ -404,7 +404,9 @@ template <int B, class S, int MS>
 __global__ void __launch_bounds__(256, 3) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
   using BR = BRec<B>;
   unsigned char* sm = smnn_dyn_smem;
-  const int K = L.K, nt = blockDim.x, t = threadIdx.x;
+  const int K = L.K, nt = blockDim.x;
+  // super-separator of this thread: identity, or grouped by reduction level
+  const int t = L.sepmap ? rf_chunk_of_thread(int(threadIdx.x), nt) : int(threadIdx.x);
   const int m = K / nt;  // separators per thread (host: K = m * nt, m <= MS)
   const int64_t g = blockIdx.x;
   S* rec = reinterpret_cast<S*>(sm);

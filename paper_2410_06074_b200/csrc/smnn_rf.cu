@@ -35,14 +35,11 @@ int rf_threads(const smnn_problem* p, int CM) {
   return nt;
 }
 
-template <int B, class Tio, class S, bool BWD>
-int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
-  constexpr int CM = RfCM<B, S>::value;
-  const int nt = rf_threads(p, CM);
-  if (nt == 0) return 0;
-  const size_t es = sizeof(Tio), ls = sizeof(S);
+template <int B, class S>
+size_t rf_smem(const smnn_problem* p, int nt, size_t es, bool bwd, RLayout& L) {
+  const size_t ls = sizeof(S);
   const int T = p->T;
-  RLayout L{};
+  L = RLayout{};
   L.nt = nt;
   L.cs = 1;
   size_t off = 0;
@@ -50,13 +47,29 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   L.off_c = take(size_t(T) * B * es + 32);
   L.off_d = take(size_t(T) * es + 32);
   L.off_s = take(size_t(T) * es + 32);
-  L.off_g = BWD ? take(size_t(T) * B * es + 32) : 0;
-  L.off_y = BWD ? take(size_t(T) * B * es + 32) : 0;
+  L.off_g = bwd ? take(size_t(T) * B * es + 32) : 0;
+  L.off_y = bwd ? take(size_t(T) * B * es + 32) : 0;
   L.lane = int(off);
   L.off_sep = take(size_t(RfSep<B, SMNN_RF_SEP>::R::N) * nt * ls + size_t(nt + 4) * 4);
   L.off_ck = 0;
   L.off_bar = take(16);
-  const size_t smem = off;
+  return off;
+}
+
+template <int B, class S>
+bool eligible_B(const smnn_problem* p, size_t es, bool bwd) {
+  const int nt = rf_threads(p, RfCM<B, S>::value);
+  RLayout L;
+  return nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024;
+}
+
+template <int B, class Tio, class S, bool BWD>
+int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
+  constexpr int CM = RfCM<B, S>::value;
+  const int nt = rf_threads(p, CM);
+  if (nt == 0) return 0;
+  RLayout L{};
+  const size_t smem = rf_smem<B, S>(p, nt, sizeof(Tio), BWD, L);
   if (smem > 200 * 1024) return 0;
   auto kern = rf_kernel<B, Tio, S, BWD, CM>;
   static std::mutex mu;
@@ -107,6 +120,17 @@ int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std
 }
 
 }  // namespace
+
+bool rf_eligible(const smnn_problem* p, bool bwd) {
+  const size_t es = p->dtype == SMNN_F64 ? 8 : 4;
+  const bool d = p->dtype != SMNN_F32;
+  switch (p->order) {
+    case 0: return d ? eligible_B<1, double>(p, es, bwd) : eligible_B<1, float>(p, es, bwd);
+    case 1: return d ? eligible_B<2, double>(p, es, bwd) : eligible_B<2, float>(p, es, bwd);
+    case 2: return d ? eligible_B<3, double>(p, es, bwd) : eligible_B<3, float>(p, es, bwd);
+    default: return d ? eligible_B<4, double>(p, es, bwd) : eligible_B<4, float>(p, es, bwd);
+  }
+}
 
 template <class Tio, class Tc>
 int rf_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err) {

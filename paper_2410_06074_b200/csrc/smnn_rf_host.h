@@ -26,4 +26,8 @@ template <class Tio, class Tc>
 int pipe_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err);
 size_t pipe_workspace_bytes(const smnn_problem* p);
 
+// Whether rf_launch / pipe_launch would take the problem (no launch).
+bool rf_eligible(const smnn_problem* p, bool bwd);
+bool pipe_eligible(const smnn_problem* p, bool bwd);
+
 }  // namespace smnn

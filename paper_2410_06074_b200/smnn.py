@@ -21,7 +21,7 @@ from . import _abi
 
 __all__ = [
     "Weights", "smnn_assemble", "smnn_factor_solve_fwd", "smnn_solve_bwd", "smnn_factor",
-    "smnn_substitute", "SMNNSolve", "smnn_solve", "workspace_bytes", "HostPlan",
+    "smnn_substitute", "SMNNSolve", "smnn_solve", "workspace_bytes", "HostPlan", "kernel_path",
 ]
 
 
@@ -81,6 +81,17 @@ def _ptr(t) -> int | None:
 
 def _stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def kernel_path(n_inst: int, T: int, order: int, n_iv: int, dtype=torch.float32, compute=None, bwd=False,
+                w: Weights = Weights()) -> str:
+    """Kernel path ("rf" | "pipe" | "checkpoint") smnn_kernel_path reports for a problem shape."""
+    code = _abi.SMNN_F64 if dtype == torch.float64 else (_abi.SMNN_F32_C64 if compute == "f64" else _abi.SMNN_F32)
+    p = _abi.smnn_problem(n_inst=n_inst, T=T, order=order, n_iv=n_iv, dtype=code, threads_per_inst=0, reserved=0,
+                          w_gov=w.gov, w_init=w.init, w_smooth=w.smooth)
+    r = _abi.load().smnn_kernel_path(ctypes.byref(p), int(bool(bwd)))
+    _abi.check(min(r, 0), "smnn_kernel_path")
+    return _abi.PATH_NAMES[r]
 
 
 def workspace_bytes(p: _abi.smnn_problem) -> int:
