@@ -686,6 +686,12 @@ struct smnn_plan {
   void *c, *d, *u, *s, *gy, *y, *gc, *gd, *gu, *gs, *ws;
   int32_t* info;
   size_t ws_bytes = 0;
+  // copy-in / compute / copy-out streams: instance groups are pipelined so that
+  // H2D of group i+1, the kernels of group i and D2H of group i-1 overlap
+  // (PCIe is full duplex; the copy engines run beside the SMs)
+  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  static constexpr int kMaxGroups = 8;
+  cudaEvent_t ev_start = nullptr, ev_in[kMaxGroups] = {}, ev_comp[kMaxGroups] = {}, ev_out = nullptr;
 };
 
 extern "C" {
@@ -836,12 +842,35 @@ int smnn_plan_create(smnn_plan** plan, const smnn_problem* p) {
   q->s = take(sz_s); q->gs = take(sz_s);
   q->info = static_cast<int32_t*>(take(sz_info));
   q->ws = take(q->ws_bytes);
+  const unsigned fl = cudaStreamNonBlocking;
+  if ((e = check_cuda(cudaStreamCreateWithFlags(&q->sin, fl), "stream")) ||
+      (e = check_cuda(cudaStreamCreateWithFlags(&q->scomp, fl), "stream")) ||
+      (e = check_cuda(cudaStreamCreateWithFlags(&q->sout, fl), "stream")) ||
+      (e = check_cuda(cudaEventCreateWithFlags(&q->ev_start, cudaEventDisableTiming), "event")) ||
+      (e = check_cuda(cudaEventCreateWithFlags(&q->ev_out, cudaEventDisableTiming), "event"))) {
+    smnn_plan_destroy(q);
+    return e;
+  }
+  for (int i = 0; i < smnn_plan::kMaxGroups; ++i)
+    if ((e = check_cuda(cudaEventCreateWithFlags(&q->ev_in[i], cudaEventDisableTiming), "event")) ||
+        (e = check_cuda(cudaEventCreateWithFlags(&q->ev_comp[i], cudaEventDisableTiming), "event"))) {
+      smnn_plan_destroy(q);
+      return e;
+    }
   *plan = q;
   return SMNN_OK;
 }
 
 int smnn_plan_destroy(smnn_plan* plan) {
   if (!plan) return SMNN_OK;
+  for (cudaStream_t st : {plan->sin, plan->scomp, plan->sout})
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : {plan->ev_start, plan->ev_out})
+    if (ev) cudaEventDestroy(ev);
+  for (int i = 0; i < smnn_plan::kMaxGroups; ++i) {
+    if (plan->ev_in[i]) cudaEventDestroy(plan->ev_in[i]);
+    if (plan->ev_comp[i]) cudaEventDestroy(plan->ev_comp[i]);
+  }
   int e = check_cuda(cudaFree(plan->buf), "cudaFree(plan)");
   delete plan;
   return e;
@@ -858,26 +887,62 @@ int smnn_plan_fwd_bwd_host(smnn_plan* q, const void* coeffs, const void* rhs, co
     return e;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t es = p->dtype == SMNN_F64 ? 8 : 4;
-  const size_t n = size_t(p->n_inst), T = size_t(p->T), b = size_t(p->order + 1);
-  const size_t bc = n * T * b * es, bd = n * T * es, bu = n * p->n_iv * es, bs = n * (T - 1) * es;
+  const int64_t n = p->n_inst;
+  const size_t T = size_t(p->T), b = size_t(p->order + 1), niv = size_t(p->n_iv);
   const cudaMemcpyKind h2d = cudaMemcpyHostToDevice, d2h = cudaMemcpyDeviceToHost;
-  if ((e = check_cuda(cudaMemcpyAsync(q->c, coeffs, bc, h2d, st), "H2D coeffs")) ||
-      (e = check_cuda(cudaMemcpyAsync(q->d, rhs, bd, h2d, st), "H2D rhs")) ||
-      (e = check_cuda(cudaMemcpyAsync(q->u, iv, bu, h2d, st), "H2D iv")) ||
-      (bs && (e = check_cuda(cudaMemcpyAsync(q->s, steps, bs, h2d, st), "H2D steps"))) ||
-      (e = check_cuda(cudaMemcpyAsync(q->gy, grad_y, bc, h2d, st), "H2D grad_y")))
+  // groups of instances, each large enough to keep the GPU busy on its own
+  const int G = int(std::max<int64_t>(1, std::min<int64_t>(smnn_plan::kMaxGroups, n / 256)));
+  auto H = [](const void* base, size_t off) { return static_cast<const char*>(base) + off; };
+  auto Hm = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
+  auto D = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
+  if ((e = check_cuda(cudaEventRecord(q->ev_start, st), "event")) ||
+      (e = check_cuda(cudaStreamWaitEvent(q->sin, q->ev_start, 0), "wait")) ||
+      (e = check_cuda(cudaStreamWaitEvent(q->scomp, q->ev_start, 0), "wait")) ||
+      (e = check_cuda(cudaStreamWaitEvent(q->sout, q->ev_start, 0), "wait")))
     return e;
-  if ((e = smnn_factor_solve_fwd(p, q->c, q->d, q->u, q->s, q->y, nullptr, q->ws, q->ws_bytes, stream))) return e;
-  if ((e = smnn_solve_bwd(p, q->c, q->d, q->u, q->s, q->y, q->gy, q->gc, q->gd, q->gu, q->gs, q->info, q->ws,
-                          q->ws_bytes, stream)))
+  for (int gi = 0; gi < G; ++gi) {
+    const int64_t i0 = n * gi / G, i1 = n * (gi + 1) / G, ni = i1 - i0;
+    const size_t oc = size_t(i0) * T * b * es, od = size_t(i0) * T * es, ou = size_t(i0) * niv * es,
+                 os = size_t(i0) * (T - 1) * es;
+    const size_t bc = size_t(ni) * T * b * es, bd = size_t(ni) * T * es, bu = size_t(ni) * niv * es,
+                 bs = size_t(ni) * (T - 1) * es;
+    if ((e = check_cuda(cudaMemcpyAsync(D(q->c, oc), H(coeffs, oc), bc, h2d, q->sin), "H2D coeffs")) ||
+        (e = check_cuda(cudaMemcpyAsync(D(q->d, od), H(rhs, od), bd, h2d, q->sin), "H2D rhs")) ||
+        (e = check_cuda(cudaMemcpyAsync(D(q->u, ou), H(iv, ou), bu, h2d, q->sin), "H2D iv")) ||
+        (bs && (e = check_cuda(cudaMemcpyAsync(D(q->s, os), H(steps, os), bs, h2d, q->sin), "H2D steps"))) ||
+        (e = check_cuda(cudaMemcpyAsync(D(q->gy, oc), H(grad_y, oc), bc, h2d, q->sin), "H2D grad_y")) ||
+        (e = check_cuda(cudaEventRecord(q->ev_in[gi], q->sin), "event")) ||
+        (e = check_cuda(cudaStreamWaitEvent(q->scomp, q->ev_in[gi], 0), "wait")))
+      return e;
+    smnn_problem pg = *p;
+    pg.n_inst = ni;
+    if ((e = smnn_factor_solve_fwd(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc), nullptr,
+                                   q->ws, q->ws_bytes, q->scomp)))
+      return e;
+    if ((e = smnn_solve_bwd(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc), D(q->gy, oc),
+                            D(q->gc, oc), D(q->gd, od), D(q->gu, ou), D(q->gs, os),
+                            q->info + i0, q->ws, q->ws_bytes, q->scomp)))
+      return e;
+    if ((e = check_cuda(cudaEventRecord(q->ev_comp[gi], q->scomp), "event")) ||
+        (e = check_cuda(cudaStreamWaitEvent(q->sout, q->ev_comp[gi], 0), "wait")) ||
+        (e = check_cuda(cudaMemcpyAsync(Hm(y, oc), D(q->y, oc), bc, d2h, q->sout), "D2H y")))
+      return e;
+    if (grad_coeffs && (e = check_cuda(cudaMemcpyAsync(Hm(grad_coeffs, oc), D(q->gc, oc), bc, d2h, q->sout), "D2H dc")))
+      return e;
+    if (grad_rhs && (e = check_cuda(cudaMemcpyAsync(Hm(grad_rhs, od), D(q->gd, od), bd, d2h, q->sout), "D2H dd")))
+      return e;
+    if (grad_iv && (e = check_cuda(cudaMemcpyAsync(Hm(grad_iv, ou), D(q->gu, ou), bu, d2h, q->sout), "D2H du")))
+      return e;
+    if (grad_steps && bs &&
+        (e = check_cuda(cudaMemcpyAsync(Hm(grad_steps, os), D(q->gs, os), bs, d2h, q->sout), "D2H ds")))
+      return e;
+    if (info && (e = check_cuda(cudaMemcpyAsync(info + i0, q->info + i0, size_t(ni) * 4, d2h, q->sout), "D2H info")))
+      return e;
+  }
+  // the caller's stream resumes after the last copy-out
+  if ((e = check_cuda(cudaEventRecord(q->ev_out, q->sout), "event")) ||
+      (e = check_cuda(cudaStreamWaitEvent(st, q->ev_out, 0), "wait")))
     return e;
-  if ((e = check_cuda(cudaMemcpyAsync(y, q->y, bc, d2h, st), "D2H y"))) return e;
-  if (grad_coeffs && (e = check_cuda(cudaMemcpyAsync(grad_coeffs, q->gc, bc, d2h, st), "D2H grad_coeffs"))) return e;
-  if (grad_rhs && (e = check_cuda(cudaMemcpyAsync(grad_rhs, q->gd, bd, d2h, st), "D2H grad_rhs"))) return e;
-  if (grad_iv && (e = check_cuda(cudaMemcpyAsync(grad_iv, q->gu, bu, d2h, st), "D2H grad_iv"))) return e;
-  if (grad_steps && bs && (e = check_cuda(cudaMemcpyAsync(grad_steps, q->gs, bs, d2h, st), "D2H grad_steps")))
-    return e;
-  if (info && (e = check_cuda(cudaMemcpyAsync(info, q->info, n * 4, d2h, st), "D2H info"))) return e;
   return SMNN_OK;
 }
 
