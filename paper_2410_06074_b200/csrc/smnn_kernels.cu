@@ -590,17 +590,19 @@ int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
 }
 
 // Kernel path of the fused calls (SMNN_PATH_*), environment SMNN_KERNEL =
-// auto (default) | rf | pipe | resident | stream.  Measured on B200: the
-// resident RF kernel wins while one CTA holds the instance (T <~ 4k); the
-// pipeline beyond it (T = 1e4: 3x the streaming kernel), except fp64
-// arithmetic at order 3 (register spills); then the checkpointing kernels.
+// auto (default) | rf | pipe | resident | stream.  Measured on B200 (profiles/):
+// with fp32 arithmetic the resident RF kernel wins while one CTA holds the
+// instance (T <~ 4k: Lorenz 9.3e9 -> 13.1e9 instance-steps/s) and the
+// pipeline beyond it (T = 1e4: 7.1e9 -> 22e9); with fp64 arithmetic their
+// register-resident factors spill and the checkpointing kernels stay faster
+// (Lorenz f64: 3.9e9 vs 3.5e9), so "auto" keeps those; rf / pipe can still be
+// forced (the parity tests run every path).
 int kernel_path(const smnn_problem* p, bool bwd) {
   const char* env = std::getenv("SMNN_KERNEL");
   const std::string mode = env ? env : "auto";
-  if ((mode == "auto" || mode == "rf") && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
-  const bool c64 = p->dtype != SMNN_F32;
-  if ((mode == "pipe" || (mode == "auto" && !(c64 && p->order >= 3))) && smnn::pipe_eligible(p, bwd))
-    return SMNN_PATH_PIPE;
+  const bool auto32 = mode == "auto" && p->dtype == SMNN_F32;
+  if ((auto32 || mode == "rf") && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
+  if ((auto32 || mode == "pipe") && smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
   return SMNN_PATH_CHECKPOINT;
 }
 

@@ -67,4 +67,5 @@ def test_kernel_path_selection(lib):
     assert kernel_path(4096, 10000, 2, 2) == "pipe"                   # north_star target
     assert kernel_path(4096, 10000, 2, 2, bwd=True) == "pipe"
     assert kernel_path(8192, 2000, 3, 3, compute="f64") == "checkpoint"  # KdV default (configs[2])
+    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "checkpoint"  # fp64: spills in rf
     assert kernel_path(2, 3, 2, 2) == "checkpoint"                    # too short to chunk

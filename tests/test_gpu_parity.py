@@ -243,3 +243,37 @@ def test_full_size_sampled(smnn, name):
     for got, ref, pert in zip(g[:4], g_ref, g_pert):
         tol = max(1e-4, 16 * rel_err(pert.numpy(), ref.numpy()))
         assert rel_err(got.cpu().numpy()[idx], ref.numpy()) < tol
+
+
+PATH_CASES = [  # (n, T, R, n_iv): every kernel path must match the oracle, forced through SMNN_KERNEL
+    (3, 64, 2, 2), (2, 1000, 2, 2), (2, 777, 1, 1), (2, 3000, 2, 2), (2, 257, 3, 4), (2, 400, 0, 1),
+]
+
+
+@pytest.mark.parametrize("mode", ["rf", "pipe", "resident", "stream"])
+@pytest.mark.parametrize("n,T,R,n_iv", PATH_CASES)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_forced_kernel_paths(smnn, monkeypatch, mode, n, T, R, n_iv, dt):
+    """fp64 parity (1e-9 floor, kappa-aware) and fp32 backward error of every
+    kernel path, including the ones "auto" does not pick for this shape."""
+    monkeypatch.setenv("SMNN_KERNEL", mode)
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    x = make_inputs(n, T, R, n_iv, dtype=dt, seed=3 * T + R)
+    gy = make_grad_y(n, T, R, dtype=dt, seed=T + 5)
+    t = to_dev(x, tdt)
+    w = smnn.Weights(*W)
+    args = (x["coeffs"], x["rhs"], x["iv"], x["steps"])
+    y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w)
+    assert int(info.abs().max()) == 0
+    g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, torch.from_numpy(gy).cuda(), w)
+    assert int(g[4].abs().max()) == 0
+    if dt == "f32":
+        yc = y.cpu().numpy()
+        for i in range(n):
+            assert backward_error(x, yc, i, W) < 64 * U32
+        return
+    tol = max(1e-9, 16 * max(kappa(x, i, W) for i in range(n)) * U64)
+    assert rel_err(y.cpu(), O.solve_instances(*args, w=W).numpy()) < tol
+    for name, got, ref in zip(("dcoeffs", "drhs", "div", "dsteps"), g[:4], O.grads_instances(*args, gy, w=W)):
+        if ref.numel():
+            assert rel_err(got.cpu(), ref.numpy()) < 4 * tol, name
