@@ -634,7 +634,12 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
   unsigned char* sm = smnn_dyn_smem;
   Tio* smT = reinterpret_cast<Tio*>(sm);
   const int nt = blockDim.x, K = nt;
-  const int k = RF_MAP ? rf_chunk_of_thread(int(threadIdx.x), K) : int(threadIdx.x);
+  // RF_MAP 2: odd chunks (the separators the first reduction level eliminates)
+  // in the first half of the CTA, even ones in the second half, so that level
+  // 1 runs one code path per warp and levels >= 2 run on half of the warps
+  const int k = RF_MAP == 1 ? rf_chunk_of_thread(int(threadIdx.x), K)
+              : RF_MAP == 2 ? (int(threadIdx.x) < K / 2 ? 2 * int(threadIdx.x) + 1 : 2 * (int(threadIdx.x) - K / 2))
+                            : int(threadIdx.x);
   const int T = a.T;
   using Q = RRec<B>;
   using R2 = typename RfSep<B, SMNN_RF_SEP>::R;
@@ -916,14 +921,31 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
     RF_STAMP(3);
     // ================================================================ pass 2
     // forward substitution with both separator values known
-    S Wp[CM - 1][B];
+    // w'_i goes to shared memory, in place over the step's consumed right-hand
+    // side input (c_i forward -- y_i overwrites it afterwards; dl/dy_i backward)
+    // when the storage type can hold it exactly, else to registers
+    constexpr bool WSM = sizeof(S) == sizeof(Tio);
+    S Wp[WSM ? 1 : CM - 1][B];
+    Tio* wS = const_cast<Tio*>(BWD ? gS : cS);
+    auto wput = [&](int i, const S (&v)[B]) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        if (WSM) wS[i * B + r] = Tio(v[r]); else Wp[WSM ? 0 : i][r] = v[r];
+      }
+    };
+    auto wget = [&](int i, S (&v)[B]) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) v[r] = WSM ? S(wS[i * B + r]) : Wp[WSM ? 0 : i][r];
+    };
     {
       S ap[2 * B - 1];
       if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
+      S wprev[B];
+      zero<B, S>(wprev);
 #pragma unroll
       for (int i = 0; i < CM - 1; ++i) {
         if (i < nint) {
-          S an[2 * B - 1], rhs[B], t[B], Nt[B];
+          S an[2 * B - 1], rhs[B], t[B], Nt[B], wi[B];
           spow<B, S>(S(sS[i]), w.s2, an);
           if (BWD) {
 #pragma unroll
@@ -942,12 +964,15 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
 #pragma unroll
             for (int r = 0; r < B; ++r) t[r] = yL[r];
           } else {
-            lltsolve<B, S>(Lr[i - 1], Wp[i - 1], t);
+            lltsolve<B, S>(Lr[i - 1], wprev, t);
           }
           rNv<B, S>(ap, t, Nt);
 #pragma unroll
           for (int r = 0; r < B; ++r) rhs[r] = sub_(rhs[r], Nt[r]);
-          llsolve<B, S>(Lr[i], rhs, Wp[i]);
+          llsolve<B, S>(Lr[i], rhs, wi);
+          wput(i, wi);
+#pragma unroll
+          for (int r = 0; r < B; ++r) wprev[r] = wi[r];
 #pragma unroll
           for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
         }
@@ -974,8 +999,10 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
           spow<B, S>(S(sS[i]), w.s2, an);
           rNtv<B, S>(an, yn, v);
           llsolve<B, S>(Lr[i], v, u);
+          S wi[B];
+          wget(i, wi);
 #pragma unroll
-          for (int r = 0; r < B; ++r) t[r] = sub_(Wp[i][r], u[r]);
+          for (int r = 0; r < B; ++r) t[r] = sub_(wi[r], u[r]);
           lltsolve<B, S>(Lr[i], t, yv);
           if (!BWD) {
 #pragma unroll

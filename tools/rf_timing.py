@@ -11,6 +11,8 @@ from paper_2410_06074_b200 import _abi
 from synth.workloads import WORKLOADS, make_workload_inputs, make_grad_y
 
 wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "lorenz"]
+if len(sys.argv) > 2:  # instance count override (e.g. 148: one CTA per SM, no contention)
+    wl = wl.with_(B=int(sys.argv[2]), D=1)
 x = make_workload_inputs(wl, seed=1)
 t = {k: torch.from_numpy(v).cuda() for k, v in x.items()}
 gy = torch.from_numpy(make_grad_y(wl.n_inst, wl.T, wl.order, dtype="f32", seed=2)).cuda()
