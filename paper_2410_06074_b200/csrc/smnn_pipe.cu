@@ -106,33 +106,99 @@ void set_smem(Kern k, size_t smem) {
   }
 }
 
+// Fork-join streams of the pipeline: the batch is split into groups whose
+// P1 -> SEP -> P2 chains run on different streams, so the latency-bound
+// separator kernel of one group overlaps the throughput-bound chunk kernels of
+// another.  One pool per device, created on first use.
+struct ForkJoin {
+  static constexpr int kMax = 4;
+  cudaStream_t s[kMax] = {};
+  cudaEvent_t fork = nullptr, join[kMax] = {};
+};
+
+ForkJoin* fork_join() {
+  static std::mutex mu;
+  static ForkJoin pools[64];
+  static bool made[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  ForkJoin& f = pools[dev];
+  if (!made[dev]) {
+    for (int i = 0; i < ForkJoin::kMax; ++i) {
+      if (cudaStreamCreateWithFlags(&f.s[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+      if (cudaEventCreateWithFlags(&f.join[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    if (cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    made[dev] = true;
+  }
+  return &f;
+}
+
+int pipe_groups(int64_t n_inst) {
+  const char* e = std::getenv("SMNN_PIPE_STREAMS");
+  const int want = e ? std::max(1, std::min(ForkJoin::kMax, std::atoi(e))) : 1;  // measured: no gain on B200
+  return int(std::max<int64_t>(1, std::min<int64_t>(want, n_inst / 512)));  // >= 512 instances per group
+}
+
 template <int B, class Tio, class S, bool BWD>
 int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
   constexpr int CM = PipeCM<B, S>::value;
   PipePlan q = plan_B<B, S>(p, sizeof(Tio), BWD);
   if (!q.ok) return 0;
-  char* ws = static_cast<char*>(a.ckpt);
-  for (PipeL* L : {&q.L1, &q.L2}) {
-    L->sep1 = ws;
-    L->ysep = ws + q.ws_sep1;
-    L->cfail = reinterpret_cast<int*>(ws + q.ws_sep1 + q.ws_ysep);
-  }
-  const unsigned grid_c = unsigned(p->n_inst * q.parts);
   auto k1 = pipe_p1_kernel<B, Tio, S, BWD, CM>;
   auto k2 = pipe_sep_kernel<B, S>;
   auto k2b = q.m2 > 4 ? pipe_sep2_kernel<B, S, 8> : pipe_sep2_kernel<B, S, 4>;
   auto k3 = pipe_p2_kernel<B, Tio, S, BWD, CM>;
   set_smem(k1, q.smem_p1);
   set_smem(k3, q.smem_p2);
-  k1<<<grid_c, q.NT, q.smem_p1, st>>>(a, q.L1);
-  if (q.sep2) {
-    set_smem(k2b, q.smem_sep);
-    k2b<<<unsigned(p->n_inst), q.K / q.m2, q.smem_sep, st>>>(q.L1, p->T, a.info);
-  } else {
-    set_smem(k2, q.smem_sep);
-    k2<<<unsigned(p->n_inst), q.K, q.smem_sep, st>>>(q.L1, p->T, a.info);
+  set_smem(q.sep2 ? k2b : k2, q.smem_sep);
+  const int G = pipe_groups(p->n_inst);
+  ForkJoin* fj = G > 1 ? fork_join() : nullptr;
+  const int groups = fj ? G : 1;
+  if (fj && cudaEventRecord(fj->fork, st) != cudaSuccess) fj = nullptr;
+  char* ws = static_cast<char*>(a.ckpt);
+  const int T = p->T, K = q.K;
+  const size_t ls = sizeof(S);
+  for (int gi = 0; gi < groups; ++gi) {
+    const int64_t i0 = p->n_inst * gi / groups, i1 = p->n_inst * (gi + 1) / groups, ni = i1 - i0;
+    if (ni <= 0) continue;
+    cudaStream_t sg = st;
+    if (fj) {
+      sg = fj->s[gi];
+      cudaStreamWaitEvent(sg, fj->fork, 0);
+    }
+    Args<Tio> ag = a;  // the group's instances [i0, i1)
+    ag.n_inst = ni;
+    ag.coeffs = a.coeffs + i0 * T * B;
+    ag.rhs = a.rhs + i0 * T;
+    ag.iv = a.iv + i0 * a.n_iv;
+    ag.steps = a.steps + i0 * (T - 1);
+    if (a.y_in) ag.y_in = a.y_in + i0 * T * B;
+    if (a.grad_y) ag.grad_y = a.grad_y + i0 * T * B;
+    if (a.y_out) ag.y_out = a.y_out + i0 * T * B;
+    if (a.g_coeffs) ag.g_coeffs = a.g_coeffs + i0 * T * B;
+    if (a.g_rhs) ag.g_rhs = a.g_rhs + i0 * T;
+    if (a.g_iv) ag.g_iv = a.g_iv + i0 * a.n_iv;
+    if (a.g_steps) ag.g_steps = a.g_steps + i0 * (T - 1);
+    int32_t* info = a.info ? a.info + i0 : nullptr;
+    for (PipeL* L : {&q.L1, &q.L2}) {
+      L->sep1 = ws + size_t(i0) * PSep<B>::N * K * ls;
+      L->ysep = ws + q.ws_sep1 + size_t(i0) * B * K * ls;
+      L->cfail = reinterpret_cast<int*>(ws + q.ws_sep1 + q.ws_ysep) + i0 * K;
+    }
+    const unsigned grid_c = unsigned(ni * q.parts);
+    k1<<<grid_c, q.NT, q.smem_p1, sg>>>(ag, q.L1);
+    if (q.sep2)
+      k2b<<<unsigned(ni), q.K / q.m2, q.smem_sep, sg>>>(q.L1, T, info);
+    else
+      k2<<<unsigned(ni), q.K, q.smem_sep, sg>>>(q.L1, T, info);
+    k3<<<grid_c, q.NT, q.smem_p2, sg>>>(ag, q.L2);
+    if (fj) {
+      cudaEventRecord(fj->join[gi], sg);
+      cudaStreamWaitEvent(st, fj->join[gi], 0);
+    }
   }
-  k3<<<grid_c, q.NT, q.smem_p2, st>>>(a, q.L2);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("pipeline launch: ") + cudaGetErrorString(e);

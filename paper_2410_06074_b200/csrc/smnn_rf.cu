@@ -48,10 +48,13 @@ size_t rf_smem(const smnn_problem* p, int nt, size_t es, bool bwd, RLayout& L) {
   L.off_d = take(size_t(T) * es + 32);
   L.off_s = take(size_t(T) * es + 32);
   L.off_g = bwd ? take(size_t(T) * B * es + 32) : 0;
-  L.off_y = bwd ? take(size_t(T) * B * es + 32) : 0;
+  const bool late_y = bwd && RF_LATE_Y;
+  L.off_y = (bwd && !late_y) ? take(size_t(T) * B * es + 32) : 0;
   L.lane = int(off);
-  L.off_sep = take(size_t(RfSep<B, SMNN_RF_SEP>::R::N) * nt * ls + size_t(nt + 4) * 4);
-  L.off_ck = 0;
+  const size_t rec = size_t(RfSep<B, SMNN_RF_SEP>::R::N) * nt * ls;
+  L.off_sep = take(late_y ? std::max(rec, size_t(T) * B * es + 32) : rec);  // late y reuses the records
+  if (late_y) L.off_y = L.off_sep;
+  L.off_ck = take(size_t(nt + 4) * 4);  // separator times + failure flag
   L.off_bar = take(16);
   return off;
 }

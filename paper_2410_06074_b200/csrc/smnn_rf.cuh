@@ -46,6 +46,14 @@ __device__ __forceinline__ int opaque(int v) { asm volatile("" : "+r"(v)); retur
 __device__ __forceinline__ float opaque(float v) { asm volatile("" : "+f"(v)); return v; }
 __device__ __forceinline__ double opaque(double v) { asm volatile("" : "+d"(v)); return v; }
 
+// Backward: stage the forward solution y only after the separator reduction,
+// into the reduction's record region (free by then), overlapped with the
+// pass-2 forward sweep -- one staging buffer less (44 -> 32 B per time point),
+// so one more CTA per SM.
+#ifndef RF_LATE_Y
+#define RF_LATE_Y (SMNN_RF_SEP != 0)
+#endif
+
 // Thread -> chunk map: 1 = grouped by reduction level (rf_chunk_of_thread), 0 = identity.
 #ifndef RF_MAP
 #define RF_MAP 0
@@ -644,7 +652,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
   using Q = RRec<B>;
   using R2 = typename RfSep<B, SMNN_RF_SEP>::R;
   S* sep = reinterpret_cast<S*>(sm + L.off_sep);  // K separator records
-  int* stime = reinterpret_cast<int*>(sep + size_t(R2::N) * nt);
+  int* stime = reinterpret_cast<int*>(sm + L.off_ck);  // after the record region
   int* sfail = stime + nt;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.off_bar);
   const Wts<S> w{opaque(splat<S>(a.wg2)), opaque(splat<S>(a.wi2)), opaque(splat<S>(a.ws2))};
@@ -664,15 +672,16 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
     const Span<Tio> ps(a.steps + tsb, T - 1);
     const Span<Tio> pg(BWD ? a.grad_y + tb : a.coeffs, BWD ? T * B : 0);
     const Span<Tio> py(BWD ? a.y_in + tb : a.coeffs, BWD ? T * B : 0);
+    constexpr bool LATE_Y = BWD && RF_LATE_Y;
     if (k == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes);
+      mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + (LATE_Y ? 0u : py.bytes));
       bulk_g2s(sm + L.off_c, pc.lo, pc.bytes, bar);
       bulk_g2s(sm + L.off_d, pd.lo, pd.bytes, bar);
       if (ps.bytes) bulk_g2s(sm + L.off_s, ps.lo, ps.bytes, bar);
       if (BWD) {
         bulk_g2s(sm + L.off_g, pg.lo, pg.bytes, bar);
-        bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
+        if (!LATE_Y) bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
       }
     }
     Grp<Tio, 1> x;  // streams as element offsets into shared memory
@@ -918,6 +927,14 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
     if (k > 0) rld_v<B, S>(sep + (k - 1) * R2::N + R2::Y, yL); else zero<B, S>(yL);
 #endif
 
+    if (LATE_Y) {  // every thread has read its separator values: the records may go
+      __syncthreads();
+      if (k == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, py.bytes);
+        bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
+      }
+    }
     RF_STAMP(3);
     // ================================================================ pass 2
     // forward substitution with both separator values known
@@ -977,6 +994,10 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
           for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
         }
       }
+    }
+    if (LATE_Y) {
+      mbar_wait(bar, parity);
+      parity ^= 1u;
     }
     // back substitution from y_{sigma_k}
     {
