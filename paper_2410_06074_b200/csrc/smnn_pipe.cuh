@@ -40,6 +40,9 @@ struct PipeCM {  // chunk capacity: P2 keeps CM - 1 factors + rhs in registers
 #ifndef SMNN_PIPE_NT
 #define SMNN_PIPE_NT 128
 #endif
+#ifndef SMNN_PIPE_P2_MINB
+#define SMNN_PIPE_P2_MINB 4
+#endif
 #ifndef SMNN_PIPE_SEP_MAX
 #define SMNN_PIPE_SEP_MAX 1024
 #endif
@@ -603,7 +606,8 @@ __global__ void __launch_bounds__(256, 3) pipe_sep2_kernel(PipeL L, int T, int32
 
 // ============================================================== P2 ========
 template <int B, class Tio, class S, bool BWD, int CM>
-__global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p2_kernel(Args<Tio> a, PipeL L) {
+__global__ void __launch_bounds__(SMNN_PIPE_NT, BWD ? SMNN_PIPE_P2_MINB : SMNN_PIPE_P2_MINB + 1)
+    pipe_p2_kernel(Args<Tio> a, PipeL L) {  // forward: 5 CTAs/SM (measured +4 %), backward: 4 (spills at 5)
   unsigned char* sm = smnn_dyn_smem;
   Tio* smT = reinterpret_cast<Tio*>(sm);
   const int T = a.T, K = L.K, tid = threadIdx.x;
@@ -673,7 +677,14 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p2_kernel(Args<Tio> a, P
 
   if (act) {
     // forward sweep: re-factor the interior and forward-substitute with y_L known
-    S Lr[CM - 1][B][B], Wp[CM - 1][B];
+    S Lr[CM - 1][B][B];
+    // w'_i in shared memory over the consumed rhs input (c_i forward, later
+    // overwritten by y_i; dl/dy_i backward) when the storage type holds it exactly
+    constexpr bool WSM = sizeof(S) == sizeof(Tio);
+    S Wp[WSM ? 1 : CM - 1][B];
+    Tio* wS = const_cast<Tio*>(BWD ? gS : cS);
+    S wprev[B];
+    zero<B, S>(wprev);
     {
       S ap[2 * B - 1];
       if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
@@ -709,10 +720,14 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p2_kernel(Args<Tio> a, P
           } else {
             S Pm[B][B];
             lPfromN<B, S>(ap, Lr[i - 1], Pm);
-            lcouple<B, S>(Pm, Wp[i - 1], M, rhs);
+            lcouple<B, S>(Pm, wprev, M, rhs);
           }
           lchol<B, S>(M, Lr[i]);
-          llsolve<B, S>(Lr[i], rhs, Wp[i]);
+          llsolve<B, S>(Lr[i], rhs, wprev);
+#pragma unroll
+          for (int r = 0; r < B; ++r) {
+            if (WSM) wS[i * B + r] = Tio(wprev[r]); else Wp[WSM ? 0 : i][r] = wprev[r];
+          }
 #pragma unroll
           for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
         }
@@ -739,7 +754,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p2_kernel(Args<Tio> a, P
         rNtv<B, S>(an, yn, v);
         llsolve<B, S>(Lr[i], v, uu);
 #pragma unroll
-        for (int r = 0; r < B; ++r) t[r] = sub_(Wp[i][r], uu[r]);
+        for (int r = 0; r < B; ++r) t[r] = sub_(WSM ? S(wS[i * B + r]) : Wp[WSM ? 0 : i][r], uu[r]);
         lltsolve<B, S>(Lr[i], t, yv);
         if (!BWD) {
 #pragma unroll
