@@ -277,3 +277,38 @@ def test_forced_kernel_paths(smnn, monkeypatch, mode, n, T, R, n_iv, dt):
     for name, got, ref in zip(("dcoeffs", "drhs", "div", "dsteps"), g[:4], O.grads_instances(*args, gy, w=W)):
         if ref.numel():
             assert rel_err(got.cpu(), ref.numpy()) < 4 * tol, name
+
+
+@pytest.mark.parametrize("name", ["lorenz", "sst", "target"])
+def test_full_size_bench_path_f32(smnn, name):
+    """The bench's own path and launch configuration (fp32 storage and
+    arithmetic: rf kernel for Lorenz / SST, three-kernel pipeline for the
+    north_star target) at BASELINE.json sizes: info == 0 and finite outputs
+    everywhere; on sampled instances the kappa-free backward error of y and
+    the fp64 oracle's y / gradients within the kappa-aware fp32 bounds."""
+    from synth.workloads import make_workload_inputs
+    wl = workload(name)
+    x = make_workload_inputs(wl, seed=1)
+    gy = make_grad_y(wl.n_inst, wl.T, wl.order, dtype="f32", seed=2)
+    t = to_dev(x, torch.float32)
+    path = smnn.kernel_path(wl.n_inst, wl.T, wl.order, wl.n_iv, torch.float32)
+    assert path == ("pipe" if name == "target" else "rf")
+    y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"])
+    g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, torch.from_numpy(gy).cuda())
+    assert int(info.abs().max()) == 0 and int(g[4].abs().max()) == 0
+    assert torch.isfinite(y).all() and all(torch.isfinite(z).all() for z in g[:4])
+    idx = np.random.default_rng(1).choice(wl.n_inst, size=2, replace=False)
+    sub = {k: v[idx] for k, v in x.items()}
+    yc = y.cpu().numpy()[idx]
+    for i in range(len(idx)):
+        assert backward_error(sub, yc, i, (1.0, 1.0, 1.0)) < 64 * U32
+    args = (sub["coeffs"], sub["rhs"], sub["iv"], sub["steps"])
+    kap = max(kappa(sub, i, (1.0, 1.0, 1.0)) for i in range(len(idx)))
+    tol = max(1e-4, 16 * kap * U32)
+    y_ref = O.solve_instances(*args).numpy()
+    assert rel_err(yc, y_ref) < tol, (kap, tol)
+    g_ref = O.grads_instances(*args, gy[idx])
+    xi = np.random.default_rng(0).choice([-1.0, 1.0], size=y_ref.shape)   # y-storage sensitivity
+    g_pert = O.grads_instances(*args, gy[idx], y=torch.from_numpy(y_ref * (1 + U32 * xi)))
+    for got, ref, pert in zip(g[:4], g_ref, g_pert):
+        assert rel_err(got.cpu().numpy()[idx], ref.numpy()) < max(4 * tol, 16 * rel_err(pert.numpy(), ref.numpy()))
