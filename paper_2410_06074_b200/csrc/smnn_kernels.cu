@@ -591,18 +591,19 @@ int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
 
 // Kernel path of the fused calls (SMNN_PATH_*), environment SMNN_KERNEL =
 // auto (default) | rf | pipe | resident | stream.  Measured on B200 (profiles/):
-// with fp32 arithmetic the resident RF kernel wins while one CTA holds the
-// instance (T <~ 4k: Lorenz 9.3e9 -> 13.1e9 instance-steps/s) and the
-// pipeline beyond it (T = 1e4: 7.1e9 -> 22e9); with fp64 arithmetic their
-// register-resident factors spill and the checkpointing kernels stay faster
-// (Lorenz f64: 3.9e9 vs 3.5e9), so "auto" keeps those; rf / pipe can still be
-// forced (the parity tests run every path).
+// fp32 arithmetic: the resident RF kernel while one CTA holds the instance
+// (T <~ 4k: Lorenz 9.3e9 -> 14.4e9 instance-steps/s), the pipeline beyond it
+// (T = 1e4: 7.1e9 -> 22e9); fp64 arithmetic: the pipeline first (its chunk
+// kernels keep fewer registers live than rf; SST f64 3.2e9 -> 6.2e9, KdV
+// f32c64 1.8e9 -> 2.8e9, Lorenz f64 2.4e9 -> 3.7e9), then rf; then the
+// checkpointing kernels.  Every path can be forced (the parity tests do).
 int kernel_path(const smnn_problem* p, bool bwd) {
   const char* env = std::getenv("SMNN_KERNEL");
   const std::string mode = env ? env : "auto";
-  const bool auto32 = mode == "auto" && p->dtype == SMNN_F32;
-  if ((auto32 || mode == "rf") && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
-  if ((auto32 || mode == "pipe") && smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
+  const bool aut = mode == "auto", f32 = p->dtype == SMNN_F32;
+  if ((mode == "rf" || (aut && f32)) && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
+  if ((mode == "pipe" || aut) && smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
+  if (aut && !f32 && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
   return SMNN_PATH_CHECKPOINT;
 }
 

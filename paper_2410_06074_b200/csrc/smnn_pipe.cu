@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <map>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -95,14 +96,17 @@ PipePlan plan_of(const smnn_problem* p, bool bwd) {
   return plan_S<double>(p, p->dtype == SMNN_F64 ? 8 : 4, bwd);
 }
 
+// The dynamic shared-memory attribute must cover the largest request made so
+// far for each kernel (keyed by the kernel's address: instantiations share a type).
 template <class Kern>
 void set_smem(Kern k, size_t smem) {
   static std::mutex mu;
-  static size_t top = 0;  // per kernel instantiation (template)
+  static std::map<const void*, size_t> top;
   std::lock_guard<std::mutex> lk(mu);
-  if (smem > top) {
+  size_t& t = top[reinterpret_cast<const void*>(k)];
+  if (smem > t) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    top = smem;
+    t = smem;
   }
 }
 

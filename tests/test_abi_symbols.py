@@ -56,9 +56,10 @@ def test_product_path_refuses_cpu_tensors():
 
 
 def test_kernel_path_selection(lib):
-    """smnn_kernel_path (host logic only): the resident RF kernel for instances
-    that fit one CTA, the three-kernel pipeline for long horizons, the
-    checkpointing kernels for fp64-arithmetic order 3 and explicit chunk counts."""
+    """smnn_kernel_path (host logic only): fp32 -- the resident RF kernel for
+    instances that fit one CTA, the three-kernel pipeline for long horizons;
+    fp64 arithmetic -- the pipeline first; the checkpointing kernels when
+    neither fits."""
     import torch
     from paper_2410_06074_b200 import kernel_path
     assert kernel_path(1536, 1000, 2, 2) == "rf"                      # Lorenz (configs[1])
@@ -66,6 +67,7 @@ def test_kernel_path_selection(lib):
     assert kernel_path(4096, 1461, 2, 2) == "rf"                      # SST (configs[3])
     assert kernel_path(4096, 10000, 2, 2) == "pipe"                   # north_star target
     assert kernel_path(4096, 10000, 2, 2, bwd=True) == "pipe"
-    assert kernel_path(8192, 2000, 3, 3, compute="f64") == "checkpoint"  # KdV default (configs[2])
-    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "checkpoint"  # fp64: spills in rf
+    assert kernel_path(8192, 2000, 3, 3, compute="f64") == "pipe"     # KdV default (configs[2])
+    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "pipe"  # fp64: pipeline before rf
+    assert kernel_path(4096, 10000, 2, 2, dtype=torch.float64) == "checkpoint"  # K > 1024 separators
     assert kernel_path(2, 3, 2, 2) == "checkpoint"                    # too short to chunk
