@@ -37,14 +37,18 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
   // chunks: a multiple of 32 (no idle lanes in the chunk kernels), each of
   // 2..CM points (chunk_begin spreads the remainder)
   int K = std::min(((T + CM - 1) / CM + 31) / 32 * 32, T / 2);
-  if (K > 256) K = std::min((K + 127) / 128 * 128, T / 2);  // large K: 4 separators per thread (sep2)
+  if (K > 256) {  // large K: sep2 with 4 (K <= 1024) or 8 separators per thread, K / m <= 256 threads
+    const int q128 = K > 1024 ? 256 : 128;
+    K = std::min((K + q128 - 1) / q128 * q128, T / 2);
+  }
   if (K < 1 || K > SMNN_PIPE_SEP_MAX || (T + K - 1) / K > CM) return q;
   q.sep2 = K > 256 && K % 128 == 0;
-  {
+  if (q.sep2) {  // separators per thread: 4, or 8 when K/4 would exceed 256 threads
     const char* e = std::getenv("SMNN_PIPE_M");
-    q.m2 = e ? std::max(2, std::min(8, std::atoi(e))) : 4;
-    while (q.m2 > 2 && (K % (32 * q.m2) != 0 || K / q.m2 > 256)) q.m2 = (q.m2 == 8) ? 4 : q.m2 - 1;
+    q.m2 = e ? (std::atoi(e) > 4 ? 8 : 4) : (K / 4 > 256 ? 8 : 4);
+    if (K % (32 * q.m2) != 0 || K / q.m2 > 256) q.sep2 = false;
   }
+  if (K > 256 && !q.sep2) return q;
   const size_t ls = sizeof(S);
   q.K = K;
   q.CM = CM;

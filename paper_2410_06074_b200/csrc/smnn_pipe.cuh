@@ -44,7 +44,7 @@ struct PipeCM {  // chunk capacity: P2 keeps CM - 1 factors + rhs in registers
 #define SMNN_PIPE_P2_MINB 4
 #endif
 #ifndef SMNN_PIPE_SEP_MAX
-#define SMNN_PIPE_SEP_MAX 1024
+#define SMNN_PIPE_SEP_MAX 2048
 #endif
 
 template <int B>
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p1_kernel(Args<Tio> a, P
 
 // ============================================================== SEP =======
 template <int B, class S>
-__global__ void __launch_bounds__(SMNN_PIPE_SEP_MAX, 1) pipe_sep_kernel(PipeL L, int T, int32_t* info) {
+__global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_t* info) {  // K <= 256 (larger K: sep2)
   using Q = PSep<B>;
   using BR = BRec<B>;
   unsigned char* sm = smnn_dyn_smem;

@@ -69,5 +69,6 @@ def test_kernel_path_selection(lib):
     assert kernel_path(4096, 10000, 2, 2, bwd=True) == "pipe"
     assert kernel_path(8192, 2000, 3, 3, compute="f64") == "pipe"     # KdV default (configs[2])
     assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "pipe"  # fp64: pipeline before rf
-    assert kernel_path(4096, 10000, 2, 2, dtype=torch.float64) == "checkpoint"  # K > 1024 separators
+    assert kernel_path(4096, 10000, 2, 2, dtype=torch.float64) == "pipe"  # 2048 separators: 8 per thread
+    assert kernel_path(64, 100000, 2, 2, dtype=torch.float64) == "checkpoint"  # > 2048 separators
     assert kernel_path(2, 3, 2, 2) == "checkpoint"                    # too short to chunk
