@@ -31,10 +31,19 @@
 
 namespace smnn {
 
+// P2 register segment: the factors of up to HM interior points stay in registers.
 template <int B, class S>
-struct PipeCM {  // chunk capacity: P2 keeps CM - 1 factors + rhs in registers
+struct PipeHM {
   static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 12 : B == 2 ? 8 : B == 3 ? 5 : 4)
-                                              : (B == 1 ? 24 : B == 2 ? 14 : B == 3 ? 10 : 7);
+                                              : (B == 1 ? 23 : B == 2 ? 13 : B == 3 ? 9 : 6);
+};
+// Chunk capacity (points).  fp32: one segment (HM + 1 points; measured best --
+// splitting costs a second factorisation of the first segment, more than the
+// shorter separator system saves); fp64: two segments (2 HM points: fewer
+// separators; measured +7..26 % on Lorenz / target / KdV).
+template <int B, class S>
+struct PipeCM {
+  static constexpr int value = sizeof(S) >= 8 ? 2 * PipeHM<B, S>::value : PipeHM<B, S>::value + 1;
 };
 
 #ifndef SMNN_PIPE_NT
@@ -604,6 +613,102 @@ __global__ void __launch_bounds__(256, 3) pipe_sep2_kernel(PipeL L, int T, int32
   if (t == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
 }
 
+
+// One segment [i0, i0 + len) of a chunk interior (len <= HM) in pass 2: forward
+// sweep re-factoring M from the state (Ls, ws) = (L, w') at step i0 - 1 (from
+// the chunk start -- initial-value rows, rhs -= N_{f-1} y_L -- when i0 == 0),
+// then, if STORE, back substitution from (yn, yfn) = (y, y_fwd) at step
+// i0 + len, writing the outputs and returning (yn, yfn) at step i0.  Without
+// STORE the sweep only runs through and returns the state at the last step.
+template <int B, class Tio, class S, bool BWD, int HM, bool STORE>
+__device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, int k, int f, int i0, int len,
+                                       const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS, Tio* wS,
+                                       const S (&yL)[B], S (&Ls)[B][B], S (&ws)[B], S (&yn)[B], S (&yfn)[B]) {
+  constexpr bool WSM = sizeof(S) == sizeof(Tio);
+  S Lr[STORE ? HM : 1][B][B];
+  S Wp[(STORE && !WSM) ? HM : 1][B];
+  S ap[2 * B - 1];
+  if (i0 > 0 || k > 0) spow<B, S>(S(sS[i0 - 1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
+#pragma unroll
+  for (int q = 0; q < HM; ++q) {
+    if (q < len) {
+      const int i = i0 + q;
+      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
+      spow<B, S>(S(sS[i]), w.s2, an);
+      lassemble<B, S>(c, w.g2, ap, an, M, wc);
+      if (BWD) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
+      } else {
+        const S d = S(dS[i]);
+#pragma unroll
+        for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
+      }
+      if (i == 0) {  // chunk start (q == 0, i0 == 0)
+        if (k == 0) {
+#pragma unroll
+          for (int r = 0; r < B; ++r)
+            if (r < x.n_iv) {
+              if (!BWD) rhs[r] = fma_(w.i2, S(x.u[0][r]), rhs[r]);
+              M[r][r] = add_(M[r][r], w.i2);
+            }
+        }
+        S Nt[B];  // rhs -= N_{f-1} y_L
+        rNv<B, S>(ap, yL, Nt);
+#pragma unroll
+        for (int r = 0; r < B; ++r) rhs[r] = sub_(rhs[r], Nt[r]);
+      } else {
+        S Pm[B][B];
+        lPfromN<B, S>(ap, (STORE && q > 0) ? Lr[STORE ? (q > 0 ? q - 1 : 0) : 0] : Ls, Pm);
+        lcouple<B, S>(Pm, ws, M, rhs);
+      }
+      S Lc[B][B];
+      lchol<B, S>(M, Lc);
+      llsolve<B, S>(Lc, rhs, ws);
+      if (STORE) {
+        rcopyL<B, S>(Lc, Lr[STORE ? q : 0]);
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          if (WSM) wS[i * B + r] = Tio(ws[r]); else Wp[(STORE && !WSM) ? q : 0][r] = ws[r];
+        }
+      } else {
+        rcopyL<B, S>(Lc, Ls);
+      }
+#pragma unroll
+      for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+    }
+  }
+  if (!STORE) return;
+#pragma unroll
+  for (int q = HM - 1; q >= 0; --q) {
+    if (q < len) {
+      const int i = i0 + q, j = f + i;
+      S an[2 * B - 1], v[B], uu[B], t[B], yv[B];
+      spow<B, S>(S(sS[i]), w.s2, an);
+      rNtv<B, S>(an, yn, v);
+      llsolve<B, S>(Lr[STORE ? q : 0], v, uu);
+#pragma unroll
+      for (int r = 0; r < B; ++r) t[r] = sub_(WSM ? S(wS[i * B + r]) : Wp[(STORE && !WSM) ? q : 0][r], uu[r]);
+      lltsolve<B, S>(Lr[STORE ? q : 0], t, yv);
+      if (!BWD) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[r]);
+      } else {
+        S yf[B];
+        ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
+        lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv, yf);
+        if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv, yf, yn, yfn));
+#pragma unroll
+        for (int r = 0; r < B; ++r) yfn[r] = yf[r];
+      }
+#pragma unroll
+      for (int r = 0; r < B; ++r) yn[r] = yv[r];
+    }
+  }
+}
+
 // ============================================================== P2 ========
 template <int B, class Tio, class S, bool BWD, int CM>
 __global__ void __launch_bounds__(SMNN_PIPE_NT, BWD ? SMNN_PIPE_P2_MINB : SMNN_PIPE_P2_MINB + 1)
@@ -676,68 +781,19 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, BWD ? SMNN_PIPE_P2_MINB : SMNN_P
   mbar_wait(bar, 0);
 
   if (act) {
-    // forward sweep: re-factor the interior and forward-substitute with y_L known
-    S Lr[CM - 1][B][B];
-    // w'_i in shared memory over the consumed rhs input (c_i forward, later
-    // overwritten by y_i; dl/dy_i backward) when the storage type holds it exactly
-    constexpr bool WSM = sizeof(S) == sizeof(Tio);
-    S Wp[WSM ? 1 : CM - 1][B];
+    // outputs at the separator, then the interior in (at most) two register
+    // segments: a chunk longer than HM is split as [0, h) + [h, nint) with the
+    // second segment HM long; [0, h) is factored twice (run-through to reach
+    // the state at h - 1, then stored for its back substitution).
+    constexpr int HM = PipeHM<B, S>::value;
+    static_assert(CM - 1 <= 2 * HM, "two segments must cover a chunk");
     Tio* wS = const_cast<Tio*>(BWD ? gS : cS);
-    S wprev[B];
-    zero<B, S>(wprev);
-    {
-      S ap[2 * B - 1];
-      if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
-#pragma unroll
-      for (int i = 0; i < CM - 1; ++i) {
-        if (i < nint) {
-          S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
-#pragma unroll
-          for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
-          spow<B, S>(S(sS[i]), w.s2, an);
-          lassemble<B, S>(c, w.g2, ap, an, M, wc);
-          if (BWD) {
-#pragma unroll
-            for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
-          } else {
-            const S d = S(dS[i]);
-#pragma unroll
-            for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
-          }
-          if (i == 0) {
-            if (k == 0) {
-#pragma unroll
-              for (int r = 0; r < B; ++r)
-                if (r < a.n_iv) {
-                  if (!BWD) rhs[r] = fma_(w.i2, S(x.u[0][r]), rhs[r]);
-                  M[r][r] = add_(M[r][r], w.i2);
-                }
-            }
-            S Nt[B];  // rhs -= N_{f-1} y_L
-            rNv<B, S>(ap, yL, Nt);
-#pragma unroll
-            for (int r = 0; r < B; ++r) rhs[r] = sub_(rhs[r], Nt[r]);
-          } else {
-            S Pm[B][B];
-            lPfromN<B, S>(ap, Lr[i - 1], Pm);
-            lcouple<B, S>(Pm, wprev, M, rhs);
-          }
-          lchol<B, S>(M, Lr[i]);
-          llsolve<B, S>(Lr[i], rhs, wprev);
-#pragma unroll
-          for (int r = 0; r < B; ++r) {
-            if (WSM) wS[i * B + r] = Tio(wprev[r]); else Wp[WSM ? 0 : i][r] = wprev[r];
-          }
-#pragma unroll
-          for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
-        }
-      }
-    }
-    // back substitution from y_{sigma_k} (as the RF kernel's pass 2)
-    S yn[B], yfn[B];
+    S yn[B], yfn[B], Ls[B][B], ws[B];
 #pragma unroll
     for (int r = 0; r < B; ++r) yn[r] = yR[r];
     zero<B, S>(yfn);
+    zero<B, S>(Ls);
+    zero<B, S>(ws);
     if (!BWD) {
 #pragma unroll
       for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, sig * B + r, yR[r]);
@@ -745,31 +801,15 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, BWD ? SMNN_PIPE_P2_MINB : SMNN_P
       ldlv<B, S, Tio, 1, true>(x.yin, sig * B, yfn);
       lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR, yfn);
     }
-#pragma unroll
-    for (int i = CM - 2; i >= 0; --i) {
-      if (i < nint) {
-        const int j = f + i;
-        S an[2 * B - 1], v[B], uu[B], t[B], yv[B];
-        spow<B, S>(S(sS[i]), w.s2, an);
-        rNtv<B, S>(an, yn, v);
-        llsolve<B, S>(Lr[i], v, uu);
-#pragma unroll
-        for (int r = 0; r < B; ++r) t[r] = sub_(WSM ? S(wS[i * B + r]) : Wp[WSM ? 0 : i][r], uu[r]);
-        lltsolve<B, S>(Lr[i], t, yv);
-        if (!BWD) {
-#pragma unroll
-          for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[r]);
-        } else {
-          S yf[B];
-          ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
-          lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv, yf);
-          if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv, yf, yn, yfn));
-#pragma unroll
-          for (int r = 0; r < B; ++r) yfn[r] = yf[r];
-        }
-#pragma unroll
-        for (int r = 0; r < B; ++r) yn[r] = yv[r];
-      }
+    if (CM - 1 <= HM || nint <= HM) {
+      p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, 0, nint, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+    } else {
+      const int h = nint - HM;
+      p2_seg<B, Tio, S, BWD, HM, false>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+      p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, h, HM, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+      zero<B, S>(Ls);
+      zero<B, S>(ws);
+      p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
     }
     if (BWD && k > 0 && x.gs.on) {  // interval (sigma_{k-1}, f)
       S yfm[B], am[2 * B - 1];
