@@ -31,21 +31,6 @@
 
 namespace smnn {
 
-// P2 register segment: the factors of up to HM interior points stay in registers.
-template <int B, class S>
-struct PipeHM {
-  static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 12 : B == 2 ? 8 : B == 3 ? 5 : 4)
-                                              : (B == 1 ? 23 : B == 2 ? 13 : B == 3 ? 9 : 6);
-};
-// Chunk capacity (points).  fp32: one segment (HM + 1 points; measured best --
-// splitting costs a second factorisation of the first segment, more than the
-// shorter separator system saves); fp64: two segments (2 HM points: fewer
-// separators; measured +7..26 % on Lorenz / target / KdV).
-template <int B, class S>
-struct PipeCM {
-  static constexpr int value = sizeof(S) >= 8 ? 2 * PipeHM<B, S>::value : PipeHM<B, S>::value + 1;
-};
-
 #ifndef SMNN_PIPE_NT
 #define SMNN_PIPE_NT 128
 #endif
@@ -131,123 +116,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, 4) pipe_p1_kernel(Args<Tio> a, P
 
   S Dsep[B][B], Rsep[B], Arl[B][B], All[B][B], rl[B];
   bool bad = false;
-  if (act) {
-  S ap[2 * B - 1];
-  if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
-  S Lc[B][B], wv[B], X[B][B];
-  zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
-  S sg = splat<S>(1.0);
-#pragma unroll
-  for (int i = 0; i < CM - 1; ++i) {
-    if (i < nint) {
-      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
-#pragma unroll
-      for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
-      spow<B, S>(S(sS[i]), w.s2, an);
-      lassemble<B, S>(c, w.g2, ap, an, M, wc);
-      if (BWD) {
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
-      } else {
-        const S d = S(dS[i]);
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
-      }
-      if (i == 0 && k == 0) {  // initial-value rows at t = 0
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-          if (r < a.n_iv) {
-            if (!BWD) rhs[r] = fma_(w.i2, S(u[r]), rhs[r]);
-            M[r][r] = add_(M[r][r], w.i2);
-          }
-      }
-      if (i == 0) {
-        lchol<B, S>(M, Lc);
-        llsolve<B, S>(Lc, rhs, wv);
-        S NL[B][B];  // spike X_f = L_f^{-1} N_{f-1} (zero for k = 0: ap = 0)
-        lN<B, S>(ap, NL);
-        lleft<B, S>(Lc, NL, X);
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-#pragma unroll
-          for (int q = 0; q <= r; ++q) {
-            S acc = mul_(X[0][r], X[0][q]);
-#pragma unroll
-            for (int m = 1; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
-            All[r][q] = acc;
-          }
-          S acc = mul_(X[0][r], wv[0]);
-#pragma unroll
-          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
-          rl[r] = acc;
-        }
-      } else {
-        S Pm[B][B];
-        lPfromN<B, S>(ap, Lc, Pm);  // P_{j-1} = N_{j-1} L_{j-1}^{-T}
-        lcouple<B, S>(Pm, wv, M, rhs);
-        lchol<B, S>(M, Lc);
-        llsolve<B, S>(Lc, rhs, wv);
-        S Y[B][B];  // spike X_j = -L_j^{-1} P_{j-1} X_{j-1}, carried with sign sg
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-#pragma unroll
-          for (int q = 0; q < B; ++q) {
-            S acc = mul_(Pm[r][0], X[0][q]);
-#pragma unroll
-            for (int m = 1; m < B; ++m) acc = fma_(Pm[r][m], X[m][q], acc);
-            Y[r][q] = acc;
-          }
-        lleft<B, S>(Lc, Y, X);
-        sg = neg_(sg);
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-#pragma unroll
-          for (int q = 0; q <= r; ++q) {
-            S acc = All[r][q];
-#pragma unroll
-            for (int m = 0; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
-            All[r][q] = acc;
-          }
-          S acc = mul_(X[0][r], wv[0]);
-#pragma unroll
-          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
-          rl[r] = fma_(sg, acc, rl[r]);
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
-    }
-  }
-  // one pivot check per chunk: a breakdown leaves a non-finite last factor
-  bad = bad_(splat<S>(1.0) / Lc[B - 1][B - 1]) != 0;
-  {  // Schur complement of the interior onto (sigma_{k-1}, sigma_k); ap = a(s_l)
-    S Pl[B][B];
-    lPfromN<B, S>(ap, Lc, Pl);
-#pragma unroll
-    for (int r = 0; r < B; ++r)
-#pragma unroll
-      for (int q = 0; q < B; ++q) {
-        S a2 = mul_(Pl[r][0], X[0][q]);
-#pragma unroll
-        for (int m = 1; m < B; ++m) a2 = fma_(Pl[r][m], X[m][q], a2);
-        Arl[r][q] = mul_(neg_(sg), a2);
-      }
-    S c[B], an[2 * B - 1], wc[B];
-#pragma unroll
-    for (int r = 0; r < B; ++r) c[r] = S(cS[nint * B + r]);
-    if (k + 1 < K) spow<B, S>(S(sS[nint]), w.s2, an); else zero<2 * B - 1, S>(an);
-    lassemble<B, S>(c, w.g2, ap, an, Dsep, wc);
-    if (BWD) {
-#pragma unroll
-      for (int r = 0; r < B; ++r) Rsep[r] = S(gS[nint * B + r]);
-    } else {
-      const S d = S(dS[nint]);
-#pragma unroll
-      for (int r = 0; r < B; ++r) Rsep[r] = mul_(wc[r], d);
-    }
-    lcouple<B, S>(Pl, wv, Dsep, Rsep);
-  }
-  }  // act
+  if (act) bad = p1_chunk<B, Tio, S, BWD, CM>(w, a.n_iv, u, k, K, nint, cS, dS, sS, gS, Dsep, Rsep, Arl, All, rl);
   // A_ll = -sum X^T X, r_l = -sum X^T w belong to separator k - 1: hand them to
   // the left neighbour through shared memory (the staged inputs are still in
   // use, so a region of its own); a CTA's first chunk writes them to the
@@ -614,101 +483,6 @@ __global__ void __launch_bounds__(256, 3) pipe_sep2_kernel(PipeL L, int T, int32
 }
 
 
-// One segment [i0, i0 + len) of a chunk interior (len <= HM) in pass 2: forward
-// sweep re-factoring M from the state (Ls, ws) = (L, w') at step i0 - 1 (from
-// the chunk start -- initial-value rows, rhs -= N_{f-1} y_L -- when i0 == 0),
-// then, if STORE, back substitution from (yn, yfn) = (y, y_fwd) at step
-// i0 + len, writing the outputs and returning (yn, yfn) at step i0.  Without
-// STORE the sweep only runs through and returns the state at the last step.
-template <int B, class Tio, class S, bool BWD, int HM, bool STORE>
-__device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, int k, int f, int i0, int len,
-                                       const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS, Tio* wS,
-                                       const S (&yL)[B], S (&Ls)[B][B], S (&ws)[B], S (&yn)[B], S (&yfn)[B]) {
-  constexpr bool WSM = sizeof(S) == sizeof(Tio);
-  S Lr[STORE ? HM : 1][B][B];
-  S Wp[(STORE && !WSM) ? HM : 1][B];
-  S ap[2 * B - 1];
-  if (i0 > 0 || k > 0) spow<B, S>(S(sS[i0 - 1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
-#pragma unroll
-  for (int q = 0; q < HM; ++q) {
-    if (q < len) {
-      const int i = i0 + q;
-      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
-#pragma unroll
-      for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
-      spow<B, S>(S(sS[i]), w.s2, an);
-      lassemble<B, S>(c, w.g2, ap, an, M, wc);
-      if (BWD) {
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
-      } else {
-        const S d = S(dS[i]);
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
-      }
-      if (i == 0) {  // chunk start (q == 0, i0 == 0)
-        if (k == 0) {
-#pragma unroll
-          for (int r = 0; r < B; ++r)
-            if (r < x.n_iv) {
-              if (!BWD) rhs[r] = fma_(w.i2, S(x.u[0][r]), rhs[r]);
-              M[r][r] = add_(M[r][r], w.i2);
-            }
-        }
-        S Nt[B];  // rhs -= N_{f-1} y_L
-        rNv<B, S>(ap, yL, Nt);
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = sub_(rhs[r], Nt[r]);
-      } else {
-        S Pm[B][B];
-        lPfromN<B, S>(ap, (STORE && q > 0) ? Lr[STORE ? (q > 0 ? q - 1 : 0) : 0] : Ls, Pm);
-        lcouple<B, S>(Pm, ws, M, rhs);
-      }
-      S Lc[B][B];
-      lchol<B, S>(M, Lc);
-      llsolve<B, S>(Lc, rhs, ws);
-      if (STORE) {
-        rcopyL<B, S>(Lc, Lr[STORE ? q : 0]);
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-          if (WSM) wS[i * B + r] = Tio(ws[r]); else Wp[(STORE && !WSM) ? q : 0][r] = ws[r];
-        }
-      } else {
-        rcopyL<B, S>(Lc, Ls);
-      }
-#pragma unroll
-      for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
-    }
-  }
-  if (!STORE) return;
-#pragma unroll
-  for (int q = HM - 1; q >= 0; --q) {
-    if (q < len) {
-      const int i = i0 + q, j = f + i;
-      S an[2 * B - 1], v[B], uu[B], t[B], yv[B];
-      spow<B, S>(S(sS[i]), w.s2, an);
-      rNtv<B, S>(an, yn, v);
-      llsolve<B, S>(Lr[STORE ? q : 0], v, uu);
-#pragma unroll
-      for (int r = 0; r < B; ++r) t[r] = sub_(WSM ? S(wS[i * B + r]) : Wp[(STORE && !WSM) ? q : 0][r], uu[r]);
-      lltsolve<B, S>(Lr[STORE ? q : 0], t, yv);
-      if (!BWD) {
-#pragma unroll
-        for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[r]);
-      } else {
-        S yf[B];
-        ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
-        lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv, yf);
-        if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv, yf, yn, yfn));
-#pragma unroll
-        for (int r = 0; r < B; ++r) yfn[r] = yf[r];
-      }
-#pragma unroll
-      for (int r = 0; r < B; ++r) yn[r] = yv[r];
-    }
-  }
-}
-
 // ============================================================== P2 ========
 template <int B, class Tio, class S, bool BWD, int CM>
 __global__ void __launch_bounds__(SMNN_PIPE_NT, BWD ? SMNN_PIPE_P2_MINB : SMNN_PIPE_P2_MINB + 1)
@@ -780,44 +554,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, BWD ? SMNN_PIPE_P2_MINB : SMNN_P
   __syncthreads();  // barrier initialised
   mbar_wait(bar, 0);
 
-  if (act) {
-    // outputs at the separator, then the interior in (at most) two register
-    // segments: a chunk longer than HM is split as [0, h) + [h, nint) with the
-    // second segment HM long; [0, h) is factored twice (run-through to reach
-    // the state at h - 1, then stored for its back substitution).
-    constexpr int HM = PipeHM<B, S>::value;
-    static_assert(CM - 1 <= 2 * HM, "two segments must cover a chunk");
-    Tio* wS = const_cast<Tio*>(BWD ? gS : cS);
-    S yn[B], yfn[B], Ls[B][B], ws[B];
-#pragma unroll
-    for (int r = 0; r < B; ++r) yn[r] = yR[r];
-    zero<B, S>(yfn);
-    zero<B, S>(Ls);
-    zero<B, S>(ws);
-    if (!BWD) {
-#pragma unroll
-      for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, sig * B + r, yR[r]);
-    } else {
-      ldlv<B, S, Tio, 1, true>(x.yin, sig * B, yfn);
-      lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR, yfn);
-    }
-    if (CM - 1 <= HM || nint <= HM) {
-      p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, 0, nint, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
-    } else {
-      const int h = nint - HM;
-      p2_seg<B, Tio, S, BWD, HM, false>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
-      p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, h, HM, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
-      zero<B, S>(Ls);
-      zero<B, S>(ws);
-      p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
-    }
-    if (BWD && k > 0 && x.gs.on) {  // interval (sigma_{k-1}, f)
-      S yfm[B], am[2 * B - 1];
-      ldlv<B, S, Tio, 1, true>(x.yin, (f - 1) * B, yfm);
-      spow<B, S>(S(sS[-1]), w.s2, am);
-      stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL, yfm, yn, yfn));
-    }
-  }
+  if (act) p2_chunk<B, Tio, S, BWD, CM>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR);
   // ---- outputs: TMA bulk store of the aligned body, plain stores at the ends
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();

@@ -23,13 +23,13 @@ size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Chunks (= threads) per instance: the fewest multiple-of-32 count whose
 // chunks hold at most CM points, with every chunk >= 2 points (an interior).
-int rf_threads(const smnn_problem* p, int CM) {
+int rf_threads(const smnn_problem* p, int CM, int max_threads = SMNN_RF_MAX_THREADS) {
   int nt = p->threads_per_inst;
   if (nt == 0) {
     nt = (p->T + CM - 1) / CM;
     nt = ((nt + 31) / 32) * 32;
   }
-  if (nt < 32 || nt > SMNN_RF_MAX_THREADS) return 0;
+  if (nt < 32 || nt > max_threads) return 0;
   if (2 * nt > p->T) return 0;                       // every chunk needs an interior point
   if ((p->T + nt - 1) / nt > CM) return 0;           // longest chunk must fit the registers
   return nt;
@@ -59,48 +59,61 @@ size_t rf_smem(const smnn_problem* p, int nt, size_t es, bool bwd, RLayout& L) {
   return off;
 }
 
+// Segmented variant (rf_kernel<..., SEG = true>): chunks of up to 2 PipeHM + 1
+// points, at most 256 threads -- half the separators and threads per instance,
+// at the price of re-factoring in pass 2.  Measured slower on B200 (Lorenz
+// 8.5e9 vs 14.3e9: the extra factorisation and register spills outweigh the
+// shorter reduction), so only SMNN_RF_SEG=1 selects it.
+template <int B, class S>
+struct RfSegCM {
+  static constexpr int value = 2 * PipeHM<B, S>::value + 1;
+};
+
+bool seg_enabled(const smnn_problem* p) {
+  const char* e = std::getenv("SMNN_RF_SEG");
+  (void)p;
+  return e && std::atoi(e) != 0;
+}
+
+// 0: not eligible, 1: register-factor variant, 2: segmented variant
+template <int B, class S>
+int variant_B(const smnn_problem* p, size_t es, bool bwd) {
+  RLayout L;
+  if (seg_enabled(p)) {
+    const int nt = rf_threads(p, RfSegCM<B, S>::value, 256);
+    if (nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024) return 2;
+  }
+  const int nt = rf_threads(p, RfCM<B, S>::value);
+  return (nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024) ? 1 : 0;
+}
+
 template <int B, class S>
 bool eligible_B(const smnn_problem* p, size_t es, bool bwd) {
-  const int nt = rf_threads(p, RfCM<B, S>::value);
-  RLayout L;
-  return nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024;
+  return variant_B<B, S>(p, es, bwd) != 0;
 }
 
 template <int B, class Tio, class S, bool BWD>
 int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
-  constexpr int CM = RfCM<B, S>::value;
-  const int nt = rf_threads(p, CM);
-  if (nt == 0) return 0;
+  const int var = variant_B<B, S>(p, sizeof(Tio), BWD);
+  if (var == 0) return 0;
+  constexpr int CM = RfCM<B, S>::value, CMS = RfSegCM<B, S>::value;
+  const int nt = var == 2 ? rf_threads(p, CMS, 256) : rf_threads(p, CM);
   RLayout L{};
   const size_t smem = rf_smem<B, S>(p, nt, sizeof(Tio), BWD, L);
-  if (smem > 200 * 1024) return 0;
-  auto kern = rf_kernel<B, Tio, S, BWD, CM>;
-  static std::mutex mu;
-  static std::map<std::tuple<int, size_t>, int> occ_cache;
-  int occ = 0;
-  {
+  auto kern = var == 2 ? rf_kernel<B, Tio, S, BWD, CMS, true> : rf_kernel<B, Tio, S, BWD, CM, false>;
+  {  // the attribute must cover the largest request so far, per kernel
+    static std::mutex mu;
+    static std::map<const void*, size_t> top;
     std::lock_guard<std::mutex> lk(mu);
-    auto it = occ_cache.find(std::make_tuple(nt, smem));
-    if (it != occ_cache.end()) occ = it->second;
-  }
-  static size_t smem_set = 0;  // the attribute must cover the largest request so far
-  if (smem > smem_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    std::lock_guard<std::mutex> lk(mu);
-    smem_set = std::max(smem_set, smem);
-  }
-  if (occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem) != cudaSuccess || occ < 1) {
-      cudaGetLastError();
-      occ = 1;
+    size_t& t = top[reinterpret_cast<const void*>(kern)];
+    if (smem > t) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      t = smem;
     }
-    std::lock_guard<std::mutex> lk(mu);
-    occ_cache[std::make_tuple(nt, smem)] = occ;
   }
   // one CTA per instance up to 2^31 - 1 (the block scheduler balances the tail);
   // the kernel strides over instances beyond that
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p->n_inst, int64_t(INT32_MAX)));
-  (void)occ;
   Args<Tio> aa = a;
   aa.K = nt;
   kern<<<unsigned(grid), nt, smem, st>>>(aa, L);

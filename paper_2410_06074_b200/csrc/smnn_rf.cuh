@@ -22,7 +22,7 @@
 // smnn_fused.cuh, shared with the other fused kernels.
 #pragma once
 
-#include "smnn_fused.cuh"
+#include "smnn_chunk.cuh"
 
 namespace smnn {
 
@@ -79,36 +79,6 @@ __device__ __forceinline__ unsigned long long rf_now() {
 #ifndef SMNN_RF_MAX_THREADS
 #define SMNN_RF_MAX_THREADS 512
 #endif
-
-// o = N(a) v and o = N(a)^T v with N_ik = -H_ik a_{i+k} (w_s^2 S**).
-template <int B, class S>
-__device__ __forceinline__ void rNv(const S (&a)[2 * B - 1], const S (&v)[B], S (&o)[B]) {
-#pragma unroll
-  for (int i = 0; i < B; ++i) {
-    S acc = mul_(splat<S>(-Hc(i, 0)), mul_(a[i], v[0]));
-#pragma unroll
-    for (int q = 1; q < B; ++q) acc = fma_(splat<S>(-Hc(i, q)), mul_(a[i + q], v[q]), acc);
-    o[i] = acc;
-  }
-}
-template <int B, class S>
-__device__ __forceinline__ void rNtv(const S (&a)[2 * B - 1], const S (&v)[B], S (&o)[B]) {
-#pragma unroll
-  for (int q = 0; q < B; ++q) {
-    S acc = mul_(splat<S>(-Hc(0, q)), mul_(a[q], v[0]));
-#pragma unroll
-    for (int i = 1; i < B; ++i) acc = fma_(splat<S>(-Hc(i, q)), mul_(a[i + q], v[i]), acc);
-    o[q] = acc;
-  }
-}
-
-template <int B, class S>
-__device__ __forceinline__ void rcopyL(const S (&src)[B][B], S (&dst)[B][B]) {
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int q = 0; q <= i; ++q) dst[i][q] = src[i][q];
-}
 
 // ------------------------------------------------------------------ BCR ---
 // Separator records, array of structures: separator i occupies N consecutive
@@ -637,8 +607,14 @@ __device__ __forceinline__ int rf_chunk_of_thread(int t, int K) {
   return 0;
 }
 
-template <int B, class Tio, class S, bool BWD, int CM>
-__global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_kernel(Args<Tio> a, RLayout L) {
+// SEG = false: the interior factors stay in registers from pass 1 to pass 2
+// (chunks of <= CM = RfCM points).  SEG = true: pass 1 keeps nothing
+// (p1_chunk) and pass 2 re-factors in register segments (p2_chunk), so chunks
+// can be twice as long (CM = 2 PipeHM + 1): half the separators, half the
+// threads per instance, twice the instances per SM.
+template <int B, class Tio, class S, bool BWD, int CM, bool SEG = false>
+__global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMNN_RF_MIN_BLOCKS)
+    rf_kernel(Args<Tio> a, RLayout L) {
   unsigned char* sm = smnn_dyn_smem;
   Tio* smT = reinterpret_cast<Tio*>(sm);
   const int nt = blockDim.x, K = nt;
@@ -723,12 +699,19 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
     S Bsep[B][B], Csep[B][B];
 #endif
     {
+      S All[B][B], rl[B], Arl[B][B];
+      int bad = 0, badj = INT_MAX;
+      if constexpr (SEG) {
+        if (p1_chunk<B, Tio, S, BWD, CM>(w, x.n_iv, x.u[0], k, K, nint, cS, dS, sS, gS, Dsep, Rsep, Arl, All, rl)) {
+          bad = 1;
+          badj = f;
+        }
+      } else {
       S ap[2 * B - 1];
       if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
-      S Lc[B][B], wv[B], X[B][B], All[B][B], rl[B];
+      S Lc[B][B], wv[B], X[B][B];
       zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
       S sg = splat<S>(1.0);
-      int bad = 0, badj = INT_MAX;
 #pragma unroll
       for (int i = 0; i < CM - 1; ++i) {
         if (i < nint) {
@@ -818,7 +801,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
       // recurrence carries it forward): one check per chunk instead of per pivot.
       if (bad_(splat<S>(1.0) / Lc[B - 1][B - 1])) { bad = 1; badj = f; }
       // Schur complement of the interior onto (sigma_{k-1}, sigma_k); ap = a(s_l).
-      S Pl[B][B], Arl[B][B];
+      S Pl[B][B];
       lPfromN<B, S>(ap, Lc, Pl);
 #pragma unroll
       for (int r = 0; r < B; ++r) {
@@ -847,6 +830,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
         }
         lcouple<B, S>(Pl, wv, Dsep, Rsep);
       }
+      }  // !SEG
       // A_ll = -sum X^T X and r_l = -sum X^T w belong to sigma_{k-1}: hand them over.
 #pragma unroll
       for (int r = 0; r < B; ++r) {
@@ -937,6 +921,13 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
     }
     RF_STAMP(3);
     // ================================================================ pass 2
+    if constexpr (SEG) {
+      if (LATE_Y) {
+        mbar_wait(bar, parity);
+        parity ^= 1u;
+      }
+      p2_chunk<B, Tio, S, BWD, CM>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR);
+    } else {
     // forward substitution with both separator values known
     // w'_i goes to shared memory, in place over the step's consumed right-hand
     // side input (c_i forward -- y_i overwrites it afterwards; dl/dy_i backward)
@@ -1047,6 +1038,7 @@ __global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_ke
         stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL, yfm, yn, yfn));
       }
     }
+    }  // !SEG
     RF_STAMP(4);
     // ---- write the outputs back: TMA bulk store of the 16-byte aligned body,
     //      plain stores for the unaligned head / tail elements
