@@ -250,13 +250,15 @@ PATH_CASES = [  # (n, T, R, n_iv): every kernel path must match the oracle, forc
 ]
 
 
-@pytest.mark.parametrize("mode", ["rf", "pipe", "resident", "stream"])
+@pytest.mark.parametrize("mode", ["rf", "rfseg", "pipe", "resident", "stream"])
 @pytest.mark.parametrize("n,T,R,n_iv", PATH_CASES)
 @pytest.mark.parametrize("dt", ["f64", "f32"])
 def test_forced_kernel_paths(smnn, monkeypatch, mode, n, T, R, n_iv, dt):
     """fp64 parity (1e-9 floor, kappa-aware) and fp32 backward error of every
-    kernel path, including the ones "auto" does not pick for this shape."""
-    monkeypatch.setenv("SMNN_KERNEL", mode)
+    kernel path, including the ones "auto" does not pick for this shape
+    ("rfseg": the segmented rf variant, SMNN_RF_SEG=1)."""
+    monkeypatch.setenv("SMNN_KERNEL", "rf" if mode == "rfseg" else mode)
+    monkeypatch.setenv("SMNN_RF_SEG", "1" if mode == "rfseg" else "0")
     tdt = torch.float64 if dt == "f64" else torch.float32
     x = make_inputs(n, T, R, n_iv, dtype=dt, seed=3 * T + R)
     gy = make_grad_y(n, T, R, dtype=dt, seed=T + 5)
