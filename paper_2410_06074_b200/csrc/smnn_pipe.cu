@@ -168,15 +168,26 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   char* ws = static_cast<char*>(a.ckpt);
   const int T = p->T, K = q.K;
   const size_t ls = sizeof(S);
+  // stage-major launch order (all groups' P1, then SEP, then P2): a group's
+  // separator kernel becomes ready while the next group's P1 still runs
+  struct Grp3 {
+    Args<Tio> a;
+    PipeL L1, L2;
+    int32_t* info;
+    int64_t ni;
+    cudaStream_t s;
+  } gr[ForkJoin::kMax];
   for (int gi = 0; gi < groups; ++gi) {
     const int64_t i0 = p->n_inst * gi / groups, i1 = p->n_inst * (gi + 1) / groups, ni = i1 - i0;
-    if (ni <= 0) continue;
-    cudaStream_t sg = st;
+    Grp3& G3 = gr[gi];
+    G3.ni = ni;
+    G3.s = st;
     if (fj) {
-      sg = fj->s[gi];
-      cudaStreamWaitEvent(sg, fj->fork, 0);
+      G3.s = fj->s[gi];
+      cudaStreamWaitEvent(G3.s, fj->fork, 0);
     }
-    Args<Tio> ag = a;  // the group's instances [i0, i1)
+    Args<Tio>& ag = G3.a;  // the group's instances [i0, i1)
+    ag = a;
     ag.n_inst = ni;
     ag.coeffs = a.coeffs + i0 * T * B;
     ag.rhs = a.rhs + i0 * T;
@@ -189,21 +200,29 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
     if (a.g_rhs) ag.g_rhs = a.g_rhs + i0 * T;
     if (a.g_iv) ag.g_iv = a.g_iv + i0 * a.n_iv;
     if (a.g_steps) ag.g_steps = a.g_steps + i0 * (T - 1);
-    int32_t* info = a.info ? a.info + i0 : nullptr;
-    for (PipeL* L : {&q.L1, &q.L2}) {
+    G3.info = a.info ? a.info + i0 : nullptr;
+    G3.L1 = q.L1;
+    G3.L2 = q.L2;
+    for (PipeL* L : {&G3.L1, &G3.L2}) {
       L->sep1 = ws + size_t(i0) * PSep<B>::N * K * ls;
       L->ysep = ws + q.ws_sep1 + size_t(i0) * B * K * ls;
       L->cfail = reinterpret_cast<int*>(ws + q.ws_sep1 + q.ws_ysep) + i0 * K;
     }
-    const unsigned grid_c = unsigned(ni * q.parts);
-    k1<<<grid_c, q.NT, q.smem_p1, sg>>>(ag, q.L1);
+  }
+  for (int gi = 0; gi < groups; ++gi)
+    if (gr[gi].ni > 0) k1<<<unsigned(gr[gi].ni * q.parts), q.NT, q.smem_p1, gr[gi].s>>>(gr[gi].a, gr[gi].L1);
+  for (int gi = 0; gi < groups; ++gi) {
+    if (gr[gi].ni <= 0) continue;
     if (q.sep2)
-      k2b<<<unsigned(ni), q.K / q.m2, q.smem_sep, sg>>>(q.L1, T, info);
+      k2b<<<unsigned(gr[gi].ni), q.K / q.m2, q.smem_sep, gr[gi].s>>>(gr[gi].L1, T, gr[gi].info);
     else
-      k2<<<unsigned(ni), q.K, q.smem_sep, sg>>>(q.L1, T, info);
-    k3<<<grid_c, q.NT, q.smem_p2, sg>>>(ag, q.L2);
+      k2<<<unsigned(gr[gi].ni), q.K, q.smem_sep, gr[gi].s>>>(gr[gi].L1, T, gr[gi].info);
+  }
+  for (int gi = 0; gi < groups; ++gi) {
+    if (gr[gi].ni <= 0) continue;
+    k3<<<unsigned(gr[gi].ni * q.parts), q.NT, q.smem_p2, gr[gi].s>>>(gr[gi].a, gr[gi].L2);
     if (fj) {
-      cudaEventRecord(fj->join[gi], sg);
+      cudaEventRecord(fj->join[gi], gr[gi].s);
       cudaStreamWaitEvent(st, fj->join[gi], 0);
     }
   }
