@@ -693,7 +693,7 @@ struct smnn_plan {
   // H2D of group i+1, the kernels of group i and D2H of group i-1 overlap
   // (PCIe is full duplex; the copy engines run beside the SMs)
   cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
-  static constexpr int kMaxGroups = 8;
+  static constexpr int kMaxGroups = 32;
   cudaEvent_t ev_start = nullptr, ev_in[kMaxGroups] = {}, ev_comp[kMaxGroups] = {}, ev_out = nullptr;
 };
 
@@ -894,7 +894,9 @@ int smnn_plan_fwd_bwd_host(smnn_plan* q, const void* coeffs, const void* rhs, co
   const size_t T = size_t(p->T), b = size_t(p->order + 1), niv = size_t(p->n_iv);
   const cudaMemcpyKind h2d = cudaMemcpyHostToDevice, d2h = cudaMemcpyDeviceToHost;
   // groups of instances, each large enough to keep the GPU busy on its own
-  const int G = int(std::max<int64_t>(1, std::min<int64_t>(smnn_plan::kMaxGroups, n / 256)));
+  const char* eg = std::getenv("SMNN_PLAN_GROUPS");  // experiments
+  const int Gmax = eg ? std::max(1, std::min(smnn_plan::kMaxGroups, std::atoi(eg))) : 4;  // measured best on B200
+  const int G = int(std::max<int64_t>(1, std::min<int64_t>(Gmax, n / 64)));
   auto H = [](const void* base, size_t off) { return static_cast<const char*>(base) + off; };
   auto Hm = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
   auto D = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
