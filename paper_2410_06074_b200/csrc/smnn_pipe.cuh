@@ -41,13 +41,6 @@ namespace smnn {
 #define SMNN_PIPE_SEP_MAX 2048
 #endif
 
-template <int B>
-struct PSep {
-  static constexpr int LT = B * (B + 1) / 2;
-  static constexpr int D = 0, R = LT, BL = LT + B, AL = LT + B + B * B, RL = 2 * LT + B + B * B;
-  static constexpr int N = 2 * LT + 2 * B + B * B;
-};
-
 struct PipeL {
   int K;          // chunks (= separators) per instance
   int NT;         // threads per CTA of the chunk kernels
@@ -233,54 +226,6 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
 // the first m - 1 (with the spike towards super-separator t - 1, factors kept
 // in registers), the K/m super-separators j0 + m - 1 are solved by rbcr2, and
 // the owned separators are recovered by forward + back substitution.
-template <int B, class S>
-__device__ __forceinline__ void psep_ld(const S* in, int K, int NT, int j, S (&D)[B][B], S (&r)[B], S (&Bl)[B][B]) {
-  using Q = PSep<B>;
-  int e = 0;
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int q = 0; q <= i; ++q) D[i][q] = in[int64_t(Q::D + e++) * K + j];
-#pragma unroll
-  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + j];
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
-  if (j + 1 < K && (j + 1) % NT == 0) {
-    e = 0;
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-#pragma unroll
-      for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], in[int64_t(Q::AL + e++) * K + j + 1]);
-#pragma unroll
-    for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + j + 1]);
-  }
-}
-
-template <int B, class S>
-__device__ __forceinline__ void psep_ld_rb(const S* in, int K, int NT, int j, S (&r)[B], S (&Bl)[B][B]) {
-  using Q = PSep<B>;
-#pragma unroll
-  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + j];
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
-  if (j + 1 < K && (j + 1) % NT == 0) {
-#pragma unroll
-    for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + j + 1]);
-  }
-}
-template <int B, class S>
-__device__ __forceinline__ void psep_ld_b(const S* in, int K, int j, S (&Bl)[B][B]) {
-  using Q = PSep<B>;
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
-}
-
 template <int B, class S, int MS>
 __global__ void __launch_bounds__(256, 3) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
   using BR = BRec<B>;

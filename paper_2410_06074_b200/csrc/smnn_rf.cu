@@ -51,7 +51,9 @@ size_t rf_smem(const smnn_problem* p, int nt, size_t es, bool bwd, RLayout& L) {
   const bool late_y = bwd && RF_LATE_Y;
   L.off_y = (bwd && !late_y) ? take(size_t(T) * B * es + 32) : 0;
   L.lane = int(off);
-  const size_t rec = size_t(RfSep<B, SMNN_RF_SEP>::R::N) * nt * ls;
+  // separator records (rbcr2), or the one-warp solve's field-major blocks + y + lane scratch
+  const size_t wrec = (size_t(PSep<B>::N + B) * nt + 32 * (B * (B + 1) / 2 + 2 * B * B + B)) * ls;
+  const size_t rec = std::max(size_t(RfSep<B, SMNN_RF_SEP>::R::N) * nt * ls, (RF_WARP_SEP && nt <= 128) ? wrec : 0);
   L.off_sep = take(late_y ? std::max(rec, size_t(T) * B * es + 32) : rec);  // late y reuses the records
   if (late_y) L.off_y = L.off_sep;
   L.off_ck = take(size_t(nt + 4) * 4);  // separator times + failure flag

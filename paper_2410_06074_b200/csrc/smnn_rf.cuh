@@ -54,6 +54,14 @@ __device__ __forceinline__ double opaque(double v) { asm volatile("" : "+d"(v));
 #define RF_LATE_Y (SMNN_RF_SEP != 0)
 #endif
 
+// One-warp separator solve (rsep_warp: local elimination + shuffle BCR) for
+// K <= 128.  Measured slower on B200 (Lorenz 10.9e9 vs 14.4e9: one warp does
+// the whole reduction while three wait, and its registers spill next to the
+// resident factors), so off by default.
+#ifndef RF_WARP_SEP
+#define RF_WARP_SEP 0
+#endif
+
 // Thread -> chunk map: 1 = grouped by reduction level (rf_chunk_of_thread), 0 = identity.
 #ifndef RF_MAP
 #define RF_MAP 0
@@ -567,6 +575,328 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
   __syncthreads();
 }
 
+
+// ------------------------------------------------ warp-level separator solve ---
+template <class S>
+__device__ __forceinline__ S shfl_(S v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+template <int B, class S>
+__device__ __forceinline__ void shfl_m(const S (&a)[B][B], int src, S (&o)[B][B]) {
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+#pragma unroll
+    for (int j = 0; j < B; ++j) o[i][j] = shfl_(a[i][j], src);
+}
+template <int B, class S>
+__device__ __forceinline__ void shfl_v(const S (&a)[B], int src, S (&o)[B]) {
+#pragma unroll
+  for (int i = 0; i < B; ++i) o[i] = shfl_(a[i], src);
+}
+
+// The K x K separator system of one instance solved by ONE warp (all 32 lanes
+// call it): lane l owns separators l m .. l m + m - 1 (m = K / 32 <= MS),
+// eliminates the first m - 1 (block Cholesky with the spike towards
+// super-separator l - 1, as pipe_sep2_kernel), the 32 super-separators are
+// reduced by block cyclic reduction with warp shuffles -- no shared memory
+// round trip, no CTA barrier per level -- and the owned separators are
+// recovered by forward + back substitution.  in: field-major separator blocks
+// [PSep<B>::N][K] with A_ll / r_l for every separator (psep_ld NT = 1);
+// yo: [B][K] output; scratch: 32 * (B(B+1)/2 + 2 B^2 + B) values for the
+// super-separators' factors (kept for the back substitution).
+template <int B, class S, int MS>
+__device__ __forceinline__ void rsep_warp(const S* in, int K, int T, S* yo, S* scratch, int lane, int* sfail) {
+  const int m = K / 32;
+  const int j0 = lane * m, js = j0 + m - 1;
+  int cf = INT_MAX;
+  S Lr[MS - 1][B][B];
+  S Lc[B][B], wv[B], X[B][B], All[B][B], rl[B];
+  zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
+  S sg = splat<S>(1.0);
+#pragma unroll
+  for (int i = 0; i < MS - 1; ++i) {
+    if (i < m - 1) {
+      S D[B][B], r[B], Bl[B][B];
+      psep_ld<B, S>(in, K, 1, j0 + i, D, r, Bl);
+      if (i == 0) {
+        lchol<B, S>(D, Lc);
+        llsolve<B, S>(Lc, r, wv);
+        lleft<B, S>(Lc, Bl, X);
+#pragma unroll
+        for (int a = 0; a < B; ++a) {
+#pragma unroll
+          for (int q = 0; q <= a; ++q) {
+            S acc = mul_(X[0][a], X[0][q]);
+#pragma unroll
+            for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
+            All[a][q] = acc;
+          }
+          S acc = mul_(X[0][a], wv[0]);
+#pragma unroll
+          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
+          rl[a] = acc;
+        }
+      } else {
+        S Pm[B][B];
+#pragma unroll
+        for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pm[a]);
+        lcouple<B, S>(Pm, wv, D, r);
+        lchol<B, S>(D, Lc);
+        llsolve<B, S>(Lc, r, wv);
+        S Y[B][B];
+#pragma unroll
+        for (int a = 0; a < B; ++a)
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            S acc = mul_(Pm[a][0], X[0][q]);
+#pragma unroll
+            for (int mm = 1; mm < B; ++mm) acc = fma_(Pm[a][mm], X[mm][q], acc);
+            Y[a][q] = acc;
+          }
+        lleft<B, S>(Lc, Y, X);
+        sg = neg_(sg);
+#pragma unroll
+        for (int a = 0; a < B; ++a) {
+#pragma unroll
+          for (int q = 0; q <= a; ++q) {
+            S acc = All[a][q];
+#pragma unroll
+            for (int mm = 0; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
+            All[a][q] = acc;
+          }
+          S acc = mul_(X[0][a], wv[0]);
+#pragma unroll
+          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
+          rl[a] = fma_(sg, acc, rl[a]);
+        }
+      }
+      rcopyL<B, S>(Lc, Lr[i]);
+    }
+  }
+  S Ds[B][B], Rs[B], Bs[B][B], Cs[B][B];
+  {
+    S Bl[B][B];
+    psep_ld<B, S>(in, K, 1, js, Ds, Rs, Bl);
+    if (m > 1) {
+      S Pl[B][B];
+#pragma unroll
+      for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pl[a]);
+      lcouple<B, S>(Pl, wv, Ds, Rs);
+#pragma unroll
+      for (int a = 0; a < B; ++a)
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          S acc = mul_(Pl[a][0], X[0][q]);
+#pragma unroll
+          for (int mm = 1; mm < B; ++mm) acc = fma_(Pl[a][mm], X[mm][q], acc);
+          Bs[a][q] = mul_(neg_(sg), acc);
+        }
+      if (bad_(splat<S>(1.0) / Lc[B - 1][B - 1])) cf = 1 + (chunk_begin(j0 + 1, T, K) - 1);
+    } else {
+#pragma unroll
+      for (int a = 0; a < B; ++a)
+#pragma unroll
+        for (int q = 0; q < B; ++q) Bs[a][q] = Bl[a][q];
+    }
+  }
+  {  // hand-over from lane l + 1: A_ll, r_l onto this super-separator, coupling C = B_{l+1}^T
+    S Al[B][B], Bn[B][B], rr[B];
+#pragma unroll
+    for (int a = 0; a < B; ++a) {
+      rl[a] = neg_(rl[a]);
+#pragma unroll
+      for (int q = 0; q <= a; ++q) {
+        All[a][q] = neg_(All[a][q]);
+        All[q][a] = All[a][q];
+      }
+    }
+    const int src = lane + 1 < 32 ? lane + 1 : lane;
+    shfl_m<B, S>(All, src, Al);
+    shfl_m<B, S>(Bs, src, Bn);
+    shfl_v<B, S>(rl, src, rr);
+    if (lane + 1 < 32) {
+#pragma unroll
+      for (int a = 0; a < B; ++a) {
+        Rs[a] = add_(Rs[a], rr[a]);
+#pragma unroll
+        for (int q = 0; q <= a; ++q) Ds[a][q] = add_(Ds[a][q], Al[a][q]);
+#pragma unroll
+        for (int q = 0; q < B; ++q) Cs[a][q] = Bn[q][a];
+      }
+    } else {
+      zero<B, S>(Cs);
+    }
+  }
+  // ---- block cyclic reduction over the 32 lanes
+  constexpr int LT = B * (B + 1) / 2, SN = LT + 2 * B * B + B;
+  S* my = scratch + lane * SN;  // factors of this lane's elimination level: L, F, E, g
+  int myh = 0;
+  int bad = 0;
+#pragma unroll 1
+  for (int h = 1; h < 32; h <<= 1) {
+    const int lv = lane & (2 * h - 1);
+    S F[B][B], E[B][B], gv[B];
+    zero<B, S>(F); zero<B, S>(E); zero<B, S>(gv);
+    if (lv == h) {
+      S Lf[B][B];
+      bad |= lchol<B, S>(Ds, Lf);
+      lleft<B, S>(Lf, Bs, F);
+      lleft<B, S>(Lf, Cs, E);
+      llsolve<B, S>(Lf, Rs, gv);
+      rst_tri<B, S>(my, Lf);
+      rst_full<B, S>(my + LT, F);
+      rst_full<B, S>(my + LT + B * B, E);
+      rst_v<B, S>(my + LT + 2 * B * B, gv);
+      myh = h;
+    }
+    const int sl = lane - h >= 0 ? lane - h : lane, sr = lane + h < 32 ? lane + h : lane;
+    S El[B][B], Fl[B][B], gl[B], Fr[B][B], Er[B][B], gr[B];
+    shfl_m<B, S>(E, sl, El);
+    shfl_m<B, S>(F, sl, Fl);
+    shfl_v<B, S>(gv, sl, gl);
+    shfl_m<B, S>(F, sr, Fr);
+    shfl_m<B, S>(E, sr, Er);
+    shfl_v<B, S>(gv, sr, gr);
+    if (lv == 0) {
+      if (lane - h >= 0) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            S a = Ds[i][j];
+#pragma unroll
+            for (int q = 0; q < B; ++q) a = fnma_(El[q][i], El[q][j], a);
+            Ds[i][j] = a;
+          }
+          S ar = Rs[i];
+#pragma unroll
+          for (int q = 0; q < B; ++q) ar = fnma_(El[q][i], gl[q], ar);
+          Rs[i] = ar;
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            S a = mul_(El[0][i], Fl[0][j]);
+#pragma unroll
+            for (int q = 1; q < B; ++q) a = fma_(El[q][i], Fl[q][j], a);
+            Bs[i][j] = neg_(a);
+          }
+        }
+      }
+      if (lane + h < 32) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            S a = Ds[i][j];
+#pragma unroll
+            for (int q = 0; q < B; ++q) a = fnma_(Fr[q][i], Fr[q][j], a);
+            Ds[i][j] = a;
+          }
+          S ar = Rs[i];
+#pragma unroll
+          for (int q = 0; q < B; ++q) ar = fnma_(Fr[q][i], gr[q], ar);
+          Rs[i] = ar;
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            S a = mul_(Fr[0][i], Er[0][j]);
+#pragma unroll
+            for (int q = 1; q < B; ++q) a = fma_(Fr[q][i], Er[q][j], a);
+            Cs[i][j] = neg_(a);
+          }
+        }
+      } else {
+        zero<B, S>(Cs);
+      }
+    }
+  }
+  S y[B];
+  zero<B, S>(y);
+  if (lane == 0) {
+    S Lf[B][B], t[B];
+    bad |= lchol<B, S>(Ds, Lf);
+    llsolve<B, S>(Lf, Rs, t);
+    lltsolve<B, S>(Lf, t, y);
+  }
+  if (bad) cf = min(cf, 1 + (chunk_begin(js + 1, T, K) - 1));
+#pragma unroll 1
+  for (int h = 16; h >= 1; h >>= 1) {
+    const int sl = lane - h >= 0 ? lane - h : lane, sr = lane + h < 32 ? lane + h : lane;
+    S yl[B], yr[B];
+    shfl_v<B, S>(y, sl, yl);
+    shfl_v<B, S>(y, sr, yr);
+    if (myh == h) {
+      S Lf[B][B], F[B][B], t[B];
+      rld_tri<B, S>(my, Lf);
+      rld_full<B, S>(my + LT, F);
+      rld_v<B, S>(my + LT + 2 * B * B, t);
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int q = 0; q < B; ++q) t[i] = fnma_(F[i][q], yl[q], t[i]);
+      if (lane + h < 32) {
+        S E[B][B];
+        rld_full<B, S>(my + LT + B * B, E);
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int q = 0; q < B; ++q) t[i] = fnma_(E[i][q], yr[q], t[i]);
+      }
+      lltsolve<B, S>(Lf, t, y);
+    }
+  }
+  if (cf != INT_MAX) atomicMin(sfail, cf);
+  // ---- recover the owned separators
+  S yL[B];
+  shfl_v<B, S>(y, lane > 0 ? lane - 1 : 0, yL);
+  if (lane == 0) zero<B, S>(yL);
+#pragma unroll
+  for (int a = 0; a < B; ++a) yo[a * K + js] = y[a];
+  S Wp[MS - 1][B];
+#pragma unroll
+  for (int i = 0; i < MS - 1; ++i) {
+    if (i < m - 1) {
+      S r[B], Bl[B][B], tv[B], u[B];
+      psep_ld_rb<B, S>(in, K, 1, j0 + i, r, Bl);
+      if (i == 0) {
+#pragma unroll
+        for (int a = 0; a < B; ++a) tv[a] = yL[a];
+      } else {
+        lltsolve<B, S>(Lr[i - 1], Wp[i - 1], tv);
+      }
+#pragma unroll
+      for (int a = 0; a < B; ++a) {
+        S acc = r[a];
+#pragma unroll
+        for (int q = 0; q < B; ++q) acc = fnma_(Bl[a][q], tv[q], acc);
+        u[a] = acc;
+      }
+      llsolve<B, S>(Lr[i], u, Wp[i]);
+    }
+  }
+  S yn[B];
+#pragma unroll
+  for (int a = 0; a < B; ++a) yn[a] = y[a];
+#pragma unroll
+  for (int i = MS - 2; i >= 0; --i) {
+    if (i < m - 1) {
+      S Bn[B][B], v[B], u[B], tv[B], yv[B];
+      psep_ld_b<B, S>(in, K, j0 + i + 1, Bn);
+#pragma unroll
+      for (int a = 0; a < B; ++a) {
+        S acc = mul_(Bn[0][a], yn[0]);
+#pragma unroll
+        for (int q = 1; q < B; ++q) acc = fma_(Bn[q][a], yn[q], acc);
+        v[a] = acc;
+      }
+      llsolve<B, S>(Lr[i], v, u);
+#pragma unroll
+      for (int a = 0; a < B; ++a) tv[a] = sub_(Wp[i][a], u[a]);
+      lltsolve<B, S>(Lr[i], tv, yv);
+#pragma unroll
+      for (int a = 0; a < B; ++a) yo[a * K + j0 + i] = yv[a];
+#pragma unroll
+      for (int a = 0; a < B; ++a) yn[a] = yv[a];
+    }
+  }
+}
+
 template <int B, int SEP> struct RfSep { using R = BRec<B>; };
 template <int B> struct RfSep<B, 1> { using R = PRec<B>; };
 template <int B> struct RfSep<B, 0> { using R = RRec<B>; };
@@ -637,6 +967,8 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
   uint32_t parity = 0;
   const int f = chunk_begin(k, T, K), sig = chunk_begin(k + 1, T, K) - 1;
   const int nint = sig - f;  // interior points, 1 <= nint <= CM - 1 (host guarantees)
+  // separator system solved by one warp (rsep_warp) when it has <= 4 separators per lane
+  const bool wsolve = RF_WARP_SEP && SMNN_RF_SEP == 2 && K % 32 == 0 && K <= 128;
   constexpr int E = int(sizeof(Tio));
 
   for (int64_t g = blockIdx.x; g < a.n_inst; g += gridDim.x) {
@@ -870,6 +1202,29 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
     rld_v<B, S>(sep + k * Q::N + Q::Y, yR);
     if (k > 0) rld_v<B, S>(sep + (k - 1) * Q::N + Q::Y, yL); else zero<B, S>(yL);
 #else
+      if (wsolve) {  // field-major separator blocks for the one-warp solve (rsep_warp)
+        using PS = PSep<B>;
+        S* o = sep + k;
+        int e = 0;
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+          for (int q = 0; q <= r; ++q) o[(PS::D + e++) * K] = Dsep[r][q];
+#pragma unroll
+        for (int r = 0; r < B; ++r) o[(PS::R + r) * K] = Rsep[r];
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+          for (int q = 0; q < B; ++q) o[(PS::BL + r * B + q) * K] = Arl[r][q];
+        e = 0;
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+          for (int q = 0; q <= r; ++q) o[(PS::AL + e++) * K] = All[r][q];
+#pragma unroll
+        for (int r = 0; r < B; ++r) o[(PS::RL + r) * K] = rl[r];
+        if (bad) report<1>(sfail, bad, badj);
+      } else {
       S* pk = sep + k * R2::N;  // hand-over to separator k-1
       rst_tri<B, S>(pk + R2::HA, All);
       rst_full<B, S>(pk + R2::HB, Arl);
@@ -879,9 +1234,22 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
       for (int r = 0; r < B; ++r)
 #pragma unroll
         for (int q = 0; q < B; ++q) Bsep[r][q] = Arl[r][q];
+      }  // !wsolve
     }
     __syncthreads();
     RF_STAMP(2);
+    S yL[B], yR[B];
+    if (wsolve) {
+      S* yo = sep + PSep<B>::N * K;
+      if (threadIdx.x < 32)
+        rsep_warp<B, S, 4>(sep, K, T, yo, yo + B * K, int(threadIdx.x), sfail);
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        yR[r] = yo[r * K + k];
+        yL[r] = k > 0 ? yo[r * K + k - 1] : splat<S>(0.0);
+      }
+    } else {
     if (k + 1 < K) {  // the right chunk's A_ll, r_l and the coupling to sigma_{k+1}
       S Al[B][B], An[B][B], rr[B];
       const S* pn = sep + (k + 1) * R2::N;
@@ -899,7 +1267,6 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
     } else {
       zero<B, S>(Csep);
     }
-    S yL[B], yR[B];
 #if SMNN_RF_SEP == 1
     __syncthreads();  // hand-over slots are PCR buffer 0
     rpcr<B, S>(sep, K, k, stime, sfail, Dsep, Bsep, Csep, Rsep, yR);
@@ -909,6 +1276,7 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
     rld_v<B, S>(sep + k * R2::N + R2::Y, yR);
 #endif
     if (k > 0) rld_v<B, S>(sep + (k - 1) * R2::N + R2::Y, yL); else zero<B, S>(yL);
+    }  // !wsolve
 #endif
 
     if (LATE_Y) {  // every thread has read its separator values: the records may go
