@@ -34,6 +34,9 @@ namespace smnn {
 #ifndef SMNN_PIPE_NT
 #define SMNN_PIPE_NT 128
 #endif
+#ifndef SMNN_SEP2_MINB
+#define SMNN_SEP2_MINB 3
+#endif
 #ifndef SMNN_PIPE_P2_MINB
 #define SMNN_PIPE_P2_MINB 4
 #endif
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
 // in registers), the K/m super-separators j0 + m - 1 are solved by rbcr2, and
 // the owned separators are recovered by forward + back substitution.
 template <int B, class S, int MS>
-__global__ void __launch_bounds__(256, 3) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
+__global__ void __launch_bounds__(256, SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
   using BR = BRec<B>;
   unsigned char* sm = smnn_dyn_smem;
   const int K = L.K, nt = blockDim.x;
