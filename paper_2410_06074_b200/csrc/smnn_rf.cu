@@ -77,7 +77,20 @@ bool seg_enabled(const smnn_problem* p) {
   return e && std::atoi(e) != 0;
 }
 
-// 0: not eligible, 1: register-factor variant, 2: segmented variant
+// Wide register-factor variant: chunks of up to 12 points (fp32, b = 3).
+// Measured on B200: the rf kernel is fastest with ~128 chunks per instance
+// (4 warps; fewer chunks = a shorter separator reduction, more = more
+// parallel pass work) -- SST (T = 1461) 1.39e10 -> 1.73e10 with 12-point chunks
+// (128 threads instead of 192), while Lorenz (T = 1000) stays fastest with the
+// 8-point template at 128 threads (the wide template's extra registers cost
+// 13 % there).  The host takes the variant whose thread count is the smallest
+// one >= 128.
+template <int B, class S>
+struct RfCMW {
+  static constexpr int value = (B == 3 && sizeof(S) == 4) ? 12 : RfCM<B, S>::value;
+};
+
+// 0: not eligible, 1: register-factor variant, 2: segmented variant, 3: wide register-factor variant
 template <int B, class S>
 int variant_B(const smnn_problem* p, size_t es, bool bwd) {
   RLayout L;
@@ -86,7 +99,15 @@ int variant_B(const smnn_problem* p, size_t es, bool bwd) {
     if (nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024) return 2;
   }
   const int nt = rf_threads(p, RfCM<B, S>::value);
-  return (nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024) ? 1 : 0;
+  const bool ok = nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024;
+  if (RfCMW<B, S>::value != RfCM<B, S>::value) {
+    const int nw = rf_threads(p, RfCMW<B, S>::value);
+    const bool okw = nw != 0 && rf_smem<B, S>(p, nw, es, bwd, L) <= 200 * 1024;
+    // smallest thread count >= 128 (else the largest)
+    auto score = [](int n) { return n >= 128 ? n : 100000 - n; };
+    if (okw && (!ok || score(nw) < score(nt))) return 3;
+  }
+  return ok ? 1 : 0;
 }
 
 template <int B, class S>
@@ -98,11 +119,12 @@ template <int B, class Tio, class S, bool BWD>
 int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
   const int var = variant_B<B, S>(p, sizeof(Tio), BWD);
   if (var == 0) return 0;
-  constexpr int CM = RfCM<B, S>::value, CMS = RfSegCM<B, S>::value;
-  const int nt = var == 2 ? rf_threads(p, CMS, 256) : rf_threads(p, CM);
+  constexpr int CM = RfCM<B, S>::value, CMS = RfSegCM<B, S>::value, CMW = RfCMW<B, S>::value;
+  const int nt = var == 2 ? rf_threads(p, CMS, 256) : var == 3 ? rf_threads(p, CMW) : rf_threads(p, CM);
   RLayout L{};
   const size_t smem = rf_smem<B, S>(p, nt, sizeof(Tio), BWD, L);
-  auto kern = var == 2 ? rf_kernel<B, Tio, S, BWD, CMS, true> : rf_kernel<B, Tio, S, BWD, CM, false>;
+  auto kern = var == 2 ? rf_kernel<B, Tio, S, BWD, CMS, true>
+            : var == 3 ? rf_kernel<B, Tio, S, BWD, CMW, false> : rf_kernel<B, Tio, S, BWD, CM, false>;
   {  // the attribute must cover the largest request so far, per kernel
     static std::mutex mu;
     static std::map<const void*, size_t> top;

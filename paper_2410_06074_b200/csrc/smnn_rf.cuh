@@ -26,12 +26,15 @@
 
 namespace smnn {
 
+#ifndef SMNN_RF_CM3
+#define SMNN_RF_CM3 8  // fp32, order 2 (b = 3)
+#endif
 // Chunk capacity: factors of CM - 1 interior points live in registers
 // ((CM-1) * B(B+1)/2 values of S).
 template <int B, class S>
 struct RfCM {
   static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 8 : B == 2 ? 6 : B == 3 ? 3 : 2)
-                                              : (B == 1 ? 16 : B == 2 ? 12 : B == 3 ? 8 : 5);
+                                              : (B == 1 ? 16 : B == 2 ? 12 : B == 3 ? SMNN_RF_CM3 : 5);
 };
 
 // Separator solver of the RF kernel: 2 = block cyclic reduction with the blocks
