@@ -247,6 +247,7 @@ def test_full_size_sampled(smnn, name):
 
 PATH_CASES = [  # (n, T, R, n_iv): every kernel path must match the oracle, forced through SMNN_KERNEL
     (3, 64, 2, 2), (2, 1000, 2, 2), (2, 777, 1, 1), (2, 3000, 2, 2), (2, 257, 3, 4), (2, 400, 0, 1),
+    (3, 20, 2, 2), (2, 9, 1, 1), (2, 40, 3, 3), (2, 1461, 2, 2),
 ]
 
 
