@@ -72,3 +72,17 @@ def test_kernel_path_selection(lib):
     assert kernel_path(4096, 10000, 2, 2, dtype=torch.float64) == "pipe"  # 2048 separators: 8 per thread
     assert kernel_path(64, 100000, 2, 2, dtype=torch.float64) == "checkpoint"  # > 2048 separators
     assert kernel_path(2, 3, 2, 2) == "checkpoint"                    # too short to chunk
+
+
+def test_workspace_covers_the_pipeline(lib):
+    """smnn_workspace_bytes (host logic only) covers the pipeline's separator
+    workspace: per instance and chunk the 27-field separator record, y at the
+    separators and a failure flag, K = 1024 chunks
+    for the north_star target (fp32: 10-point chunks; fp64: two 5-point
+    register segments per chunk)."""
+    from paper_2410_06074_b200 import _abi
+    for dtype, es, K in ((_abi.SMNN_F32, 4, 1024), (_abi.SMNN_F64, 8, 1024)):
+        p = _abi.smnn_problem(n_inst=4096, T=10000, order=2, n_iv=2, dtype=dtype, threads_per_inst=0, reserved=0,
+                              w_gov=1, w_init=1, w_smooth=1)
+        need = 4096 * K * ((2 * 6 + 2 * 3 + 9) * es + 3 * es + 4)
+        assert lib.smnn_workspace_bytes(ctypes.byref(p)) >= need
