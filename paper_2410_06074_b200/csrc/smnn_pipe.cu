@@ -53,8 +53,7 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
   q.K = K;
   q.CM = CM;
   q.NT = std::min(SMNN_PIPE_NT, ((K + 31) / 32) * 32);
-  q.parts = (K + q.NT - 1) / q.NT;
-  const int steps = q.NT * CM + 2;  // points of one CTA range (+ s_{ta-1}, y_{ta-1})
+  int steps = 0;
   auto layout = [&](PipeL& L, bool p2) {
     size_t off = 0;
     auto take = [&](size_t bytes) { const size_t o = off; off = al16(off + bytes); return int(o); };
@@ -67,8 +66,17 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     L.off_bar = take(16);
     return off;
   };
-  q.smem_p1 = layout(q.L1, false);
-  q.smem_p2 = layout(q.L2, true);
+  // chunk-kernel CTA: 128 chunks, fewer when its staged range would exceed
+  // 56 KB (fp64 storage with long chunks: keep >= 3-4 CTAs per SM; measured
+  // 1 CTA/SM and 5x slower at order 1, T = 1e4, f64 before)
+  for (;;) {
+    steps = q.NT * CM + 2;  // points of one CTA range (+ s_{ta-1}, y_{ta-1})
+    q.smem_p1 = layout(q.L1, false);
+    q.smem_p2 = layout(q.L2, true);
+    if (q.NT <= 32 || std::max(q.smem_p1, q.smem_p2) <= 56 * 1024) break;
+    q.NT /= 2;
+  }
+  q.parts = (K + q.NT - 1) / q.NT;
   q.smem_sep = size_t(BRec<B>::N) * (q.sep2 ? K / q.m2 : K) * ls + size_t(2 * K + 4) * 4;
   if (q.smem_p1 > 200 * 1024 || q.smem_p2 > 200 * 1024 || q.smem_sep > 220 * 1024) return q;
   q.ws_sep1 = al256(size_t(p->n_inst) * PSep<B>::N * K * ls);
