@@ -43,10 +43,13 @@ __device__ __forceinline__ void rcopyL(const S (&src)[B][B], S (&dst)[B][B]) {
     for (int q = 0; q <= i; ++q) dst[i][q] = src[i][q];
 }
 
+#ifndef SMNN_PIPE_HM4D
+#define SMNN_PIPE_HM4D 4  // fp64 arithmetic, order 3 (b = 4)
+#endif
 // P2 register segment: the factors of up to HM interior points stay in registers.
 template <int B, class S>
 struct PipeHM {
-  static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 12 : B == 2 ? 8 : B == 3 ? 5 : 4)
+  static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 12 : B == 2 ? 8 : B == 3 ? 5 : SMNN_PIPE_HM4D)
                                               : (B == 1 ? 23 : B == 2 ? 13 : B == 3 ? 9 : 6);
 };
 // Chunk capacity (points).  fp32: one segment (HM + 1 points; measured best --
