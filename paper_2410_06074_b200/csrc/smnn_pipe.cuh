@@ -34,8 +34,14 @@ namespace smnn {
 #ifndef SMNN_PIPE_NT
 #define SMNN_PIPE_NT 128
 #endif
+// separator kernel residency (CTAs/SM the register budget is cut for): fp32
+// arithmetic 3, fp64 2 (fewer spills; measured target f64 8.4e9 -> 9.4e9,
+// while fp32 at 2 loses 3 %)
 #ifndef SMNN_SEP2_MINB
 #define SMNN_SEP2_MINB 3
+#endif
+#ifndef SMNN_SEP2_MINB64
+#define SMNN_SEP2_MINB64 2
 #endif
 #ifndef SMNN_PIPE_P2_MINB
 #define SMNN_PIPE_P2_MINB 4
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
 // in registers), the K/m super-separators j0 + m - 1 are solved by rbcr2, and
 // the owned separators are recovered by forward + back substitution.
 template <int B, class S, int MS>
-__global__ void __launch_bounds__(256, SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
+__global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
   using BR = BRec<B>;
   unsigned char* sm = smnn_dyn_smem;
   const int K = L.K, nt = blockDim.x;
