@@ -145,8 +145,8 @@ int smnn_substitute(const smnn_problem* p, const void* L, const void* P,
  * A plan owns device buffers for one batch of shape `p`.  fwd_bwd_host copies
  * the HOST inputs in, runs smnn_factor_solve_fwd then smnn_solve_bwd, and
  * copies y and all gradients back to HOST memory.  The batch is split into up
- * to 4 groups of instances pipelined over the plan's own copy-in, compute and
- * copy-out streams (H2D of a group overlaps the kernels of the previous one
+ * to 8 groups of instances (about one per 16 MiB of input) pipelined over the
+ * plan's own copy-in, compute and copy-out streams (H2D of a group overlaps the kernels of the previous one
  * and the D2H of the one before), ordered after the work already on `stream`,
  * and `stream` waits for the last copy-out: the call returns once the work is
  * enqueued (synchronise `stream` before reading the outputs).  Host buffers

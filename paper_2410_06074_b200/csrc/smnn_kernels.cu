@@ -895,7 +895,11 @@ int smnn_plan_fwd_bwd_host(smnn_plan* q, const void* coeffs, const void* rhs, co
   const cudaMemcpyKind h2d = cudaMemcpyHostToDevice, d2h = cudaMemcpyDeviceToHost;
   // groups of instances, each large enough to keep the GPU busy on its own
   const char* eg = std::getenv("SMNN_PLAN_GROUPS");  // experiments
-  const int Gmax = eg ? std::max(1, std::min(smnn_plan::kMaxGroups, std::atoi(eg))) : 4;  // measured best on B200
+  // default: one group per ~16 MiB of input, 1..8 groups (measured on B200:
+  // Lorenz, 49 MB in, best at 2 groups; the 1.3 GB target best at 8)
+  const size_t in_bytes = size_t(n) * T * (2 * b + 2) * es;
+  const int Gmax = eg ? std::max(1, std::min(smnn_plan::kMaxGroups, std::atoi(eg)))
+                      : int(std::max<size_t>(1, std::min<size_t>(8, in_bytes >> 24)));
   const int G = int(std::max<int64_t>(1, std::min<int64_t>(Gmax, n / 64)));
   auto H = [](const void* base, size_t off) { return static_cast<const char*>(base) + off; };
   auto Hm = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
