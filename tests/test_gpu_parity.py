@@ -197,8 +197,13 @@ def test_autograd_gradcheck(smnn):
     assert torch.autograd.gradcheck(f, (t["coeffs"], t["rhs"], t["iv"], t["steps"]), eps=1e-6, atol=1e-6, rtol=1e-5)
 
 
-def test_host_plan_matches_device(smnn):
-    n, T, R = 8, 300, 2
+@pytest.mark.parametrize("n,groups", [(8, None), (256, "3"), (300, "4")])
+def test_host_plan_matches_device(smnn, monkeypatch, n, groups):
+    """The host plan (copy-in / compute / copy-out pipelined over instance
+    groups, ragged last group included) gives the device calls' bits."""
+    if groups is not None:
+        monkeypatch.setenv("SMNN_PLAN_GROUPS", groups)
+    T, R = 300, 2
     x = make_inputs(n, T, R, 2, dtype="f32", seed=2)
     gy = make_grad_y(n, T, R, dtype="f32")
     h = {k: torch.from_numpy(v).pin_memory() for k, v in x.items()}
