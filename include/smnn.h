@@ -94,6 +94,7 @@ const char* smnn_last_error(void);
 #define SMNN_PATH_RF 1
 #define SMNN_PATH_PIPE 2
 #define SMNN_PATH_CHECKPOINT 3
+#define SMNN_PATH_X64 4
 int smnn_kernel_path(const smnn_problem* p, int bwd);
 
 /* Bytes of device workspace the fused kernels need for `p` on the current

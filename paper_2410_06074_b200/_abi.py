@@ -17,9 +17,9 @@ EXPORTED = [
     "smnn_factor_solve_fwd", "smnn_solve_bwd", "smnn_factor", "smnn_substitute",
     "smnn_plan_create", "smnn_plan_destroy", "smnn_plan_fwd_bwd_host", "smnn_kernel_path",
 ]
-SMNN_PATH_RF, SMNN_PATH_PIPE, SMNN_PATH_CHECKPOINT = 1, 2, 3
-PATH_NAMES = {1: "rf", 2: "pipe", 3: "checkpoint"}
-PATH_LAUNCHES = {1: 1, 2: 3, 3: 1}
+SMNN_PATH_RF, SMNN_PATH_PIPE, SMNN_PATH_CHECKPOINT, SMNN_PATH_X64 = 1, 2, 3, 4
+PATH_NAMES = {1: "rf", 2: "pipe", 3: "checkpoint", 4: "x64"}
+PATH_LAUNCHES = {1: 1, 2: 3, 3: 1, 4: 1}
 
 
 class smnn_problem(ctypes.Structure):

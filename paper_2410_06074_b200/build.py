@@ -12,8 +12,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libsmnn.so")
-SOURCES = ["smnn_kernels.cu", "smnn_rf.cu", "smnn_pipe.cu"]
-HEADERS = ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_chunk.cuh", "smnn_rf.cuh", "smnn_pipe.cuh", "smnn_rf_host.h", os.path.join(ROOT, "include", "smnn.h")]
+SOURCES = ["smnn_kernels.cu", "smnn_rf.cu", "smnn_pipe.cu", "smnn_x64.cu"]
+HEADERS = ["smnn_device.cuh", "smnn_tma.cuh", "smnn_x64.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_chunk.cuh", "smnn_rf.cuh", "smnn_pipe.cuh", "smnn_rf_host.h", os.path.join(ROOT, "include", "smnn.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -30,8 +30,9 @@ def nvcc() -> str:
 
 
 DEPS = {  # headers each translation unit includes
-    "smnn_kernels.cu": ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_rf_host.h"],
+    "smnn_kernels.cu": ["smnn_device.cuh", "smnn_tma.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_rf_host.h"],
     "smnn_rf.cu": ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_chunk.cuh", "smnn_rf.cuh", "smnn_rf_host.h"],
+    "smnn_x64.cu": ["smnn_device.cuh", "smnn_tma.cuh", "smnn_x64.cuh", "smnn_rf_host.h"],
     "smnn_pipe.cu": ["smnn_device.cuh", "smnn_lane.cuh", "smnn_fused.cuh", "smnn_chunk.cuh", "smnn_rf.cuh", "smnn_pipe.cuh",
                      "smnn_rf_host.h"],
 }

@@ -23,6 +23,8 @@
 #include <climits>
 
 #include "smnn_lane.cuh"
+#include "smnn_tma.cuh"
+#include "smnn_rf_host.h"
 
 #ifndef SMNN_MAX_THREADS
 #define SMNN_MAX_THREADS 256
@@ -38,28 +40,6 @@
 
 namespace smnn {
 
-template <class Tio>
-struct Args {
-  const Tio* coeffs;
-  const Tio* rhs;
-  const Tio* iv;
-  const Tio* steps;
-  const Tio* y_in;     // BWD: forward solution
-  const Tio* grad_y;   // BWD: dl/dy
-  Tio* y_out;          // FWD: solution
-  Tio* g_coeffs;       // BWD outputs (nullable)
-  Tio* g_rhs;
-  Tio* g_iv;
-  Tio* g_steps;
-  int32_t* info;       // nullable
-  void* ckpt;          // workspace, one slot per block
-  int64_t n_inst;
-  int T;
-  int n_iv;
-  int K;               // chunks per instance (<= blockDim.x)
-  int nseg_ck;         // checkpoints per chunk (slot stride)
-  double wg2, wi2, ws2;
-};
 
 template <int B>
 struct CkN {  // checkpoint: L lower (incl. inverse diagonal), w, X
@@ -130,7 +110,6 @@ __device__ __forceinline__ void report(int* fail, int bad, int t) {
     if (bad & (1 << q)) atomicMin(fail + q, t + 1);
 }
 
-extern __shared__ __align__(128) unsigned char smnn_dyn_smem[];
 
 template <class T>
 __device__ __forceinline__ T* smem_as() { return reinterpret_cast<T*>(smnn_dyn_smem); }
@@ -1142,7 +1121,6 @@ __device__ __noinline__ void lpass2(const Grp<Tio, P> x, const Wts<S> w, SepL<B,
   lpass2_body<B, Tio, S, P, BWD, G, SM, false>(x, w, Sp, ck, k, f, sig, yL, yR);
 }
 
-__device__ __forceinline__ int chunk_begin(int k, int T, int K) { return int((int64_t(k) * T) / K); }
 
 // ------------------------------------------------------------ the kernel ---
 template <int B, class S>
@@ -1264,45 +1242,7 @@ struct RLayout {
   int off_sep, off_ck, off_bar;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
-// A 16-byte aligned superset [lo, hi) of the global elements [src, src + n):
-// cp.async.bulk needs 16-byte aligned addresses and sizes.  Reading up to 15
-// bytes outside a tensor stays inside its (>= 256-byte aligned) allocation.
-template <class T>
-struct Span {
-  const T* lo;
-  uint32_t bytes;
-  int pre;  // element offset of src inside the copied span
-  __device__ Span(const T* src, int n) {
-    const uintptr_t s = reinterpret_cast<uintptr_t>(src);
-    const uintptr_t a = s & ~uintptr_t(15);
-    const uintptr_t e = (reinterpret_cast<uintptr_t>(src + n) + 15) & ~uintptr_t(15);
-    lo = reinterpret_cast<const T*>(a);
-    bytes = n > 0 ? uint32_t(e - a) : 0u;
-    pre = int((s - a) / sizeof(T));
-  }
-};
 
 template <int B, class Tio, class S, bool BWD, int G, bool CL>
 __global__ void __launch_bounds__(SMNN_MAX_THREADS, (LaneT<S>::P == 1 ? SMNN_MIN_BLOCKS : 1))

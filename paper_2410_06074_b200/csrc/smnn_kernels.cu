@@ -601,6 +601,7 @@ int kernel_path(const smnn_problem* p, bool bwd) {
   const char* env = std::getenv("SMNN_KERNEL");
   const std::string mode = env ? env : "auto";
   const bool aut = mode == "auto", f32 = p->dtype == SMNN_F32;
+  if ((mode == "x64" || (aut && !f32)) && smnn::x64_eligible(p, bwd)) return SMNN_PATH_X64;
   if ((mode == "rf" || (aut && f32)) && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
   if ((mode == "pipe" || aut) && smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
   if (aut && !f32 && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
@@ -613,6 +614,7 @@ int dispatch_fused(const smnn_problem* p, const smnn::Args<Tio>& a, cudaStream_t
     const int path = kernel_path(p, BWD);
     std::string err;
     int r = 0;
+    if (path == SMNN_PATH_X64) r = smnn::x64_launch<Tio>(p, a, BWD, st, err);
     if (path == SMNN_PATH_RF) r = smnn::rf_launch<Tio, Tc>(p, a, BWD, st, err);
     if (path == SMNN_PATH_PIPE) r = smnn::pipe_launch<Tio, Tc>(p, a, BWD, st, err);
     if (r < 0) { g_err = err; return r; }

@@ -904,25 +904,6 @@ template <int B, int SEP> struct RfSep { using R = BRec<B>; };
 template <int B> struct RfSep<B, 1> { using R = PRec<B>; };
 template <int B> struct RfSep<B, 0> { using R = RRec<B>; };
 
-template <class Tio>
-__device__ __forceinline__ void rf_store_out(Tio* dst, const Tio* src, int n, int tid, int nt) {
-  constexpr int E = int(sizeof(Tio));
-  const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst);
-  const uintptr_t ga = (g0 + 15) & ~uintptr_t(15), gb = (g0 + uintptr_t(n) * E) & ~uintptr_t(15);
-  const int head = int((ga - g0) / E);
-  const bool bulk = n * E >= 256 && gb > ga && ((smem_u32(src + head) & 15u) == 0u);
-  if (!bulk) {
-    for (int e = tid; e < n; e += nt) dst[e] = src[e];
-    return;
-  }
-  const int tail = head + int((gb - ga) / E);
-  if (tid < head) dst[tid] = src[tid];
-  if (tid < n - tail) dst[tail + tid] = src[tail + tid];
-  if (tid == 0)
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
-                 "r"(smem_u32(src + head)), "r"(uint32_t(gb - ga))
-                 : "memory");
-}
 
 // Thread -> chunk map: chunks ordered by the level at which the separator
 // reduction eliminates them (odd k first, then k = 2 mod 4, 4 mod 8, ...,

@@ -3,14 +3,37 @@
 
 #include <cuda_runtime.h>
 
+#include <stdint.h>
+
 #include <string>
 
 #include "smnn.h"
 
 namespace smnn {
 
+// Arguments of the fused kernels (device pointers; see include/smnn.h).
 template <class Tio>
-struct Args;
+struct Args {
+  const Tio* coeffs;
+  const Tio* rhs;
+  const Tio* iv;
+  const Tio* steps;
+  const Tio* y_in;     // BWD: forward solution
+  const Tio* grad_y;   // BWD: dl/dy
+  Tio* y_out;          // FWD: solution
+  Tio* g_coeffs;       // BWD outputs (nullable)
+  Tio* g_rhs;
+  Tio* g_iv;
+  Tio* g_steps;
+  int32_t* info;       // nullable
+  void* ckpt;          // workspace, one slot per block
+  int64_t n_inst;
+  int T;
+  int n_iv;
+  int K;               // chunks per instance (<= blockDim.x)
+  int nseg_ck;         // checkpoints per chunk (slot stride)
+  double wg2, wi2, ws2;
+};
 
 // Launches the RF kernel for `p` (forward or backward) when the problem fits
 // it (instance resident in shared memory, chunks within the register budget).
@@ -29,5 +52,12 @@ size_t pipe_workspace_bytes(const smnn_problem* p);
 // Whether rf_launch / pipe_launch would take the problem (no launch).
 bool rf_eligible(const smnn_problem* p, bool bwd);
 bool pipe_eligible(const smnn_problem* p, bool bwd);
+
+// Cluster-resident fp64-arithmetic path (smnn_x64.cu): SMNN_F32_C64 and
+// SMNN_F64 while one cluster of <= 16 CTAs holds an instance.  Same contract
+// as rf_launch; no workspace.
+template <class Tio>
+int x64_launch(const smnn_problem* p, const Args<Tio>& a, bool bwd, cudaStream_t st, std::string& err);
+bool x64_eligible(const smnn_problem* p, bool bwd);
 
 }  // namespace smnn
