@@ -72,8 +72,11 @@ def test_closed_forms_are_transcribed_correctly(suite):
             assert abs(d0[r][0] - ur) < 1e-6, (ode["name"], r)
 
 
-def _solve_ode(ode, dt, T):
+def _solve_ode(ode, dt, T, order=None):
+    """Solve one Appendix B.1 ODE with the oracle; `order` embeds it at a higher
+    derivative order R (zero-padded coefficients, the given initial values only)."""
     c, d, f = closed_form(ode["name"], ode["consts"], ode["u"])
+    c = list(c) + [0.0] * ((order or 0) + 1 - len(c))
     coeffs = np.tile(np.array(c), (1, T, 1))
     rhs = np.full((1, T), d)
     iv = np.array(ode["u"])[None]
@@ -83,18 +86,28 @@ def _solve_ode(ode, dt, T):
 
 
 def test_section_5_1_validation(suite):
-    """Section 5.1 setting.  Reading R6: with all importance weights
-    1 the system of Eqs. 5-10 (pinned exactly by Appendix A.1 and polynomial
-    exactness) reaches MSE < 1e-6 on 4 of the 6 ODEs; population growth
-    (y grows to 48) and the undamped oscillator land at ~1e-5 / ~1.4e-6, above
-    the paper's "< 1e-6 in all cases", whose solver settings
-    are not stated.  The weaker bound below still fails for any dropped term,
-    wrong sign or wrong index (errors then are O(1))."""
+    """Section 5.1 setting: 1,000 steps of 0.01, MSE < 1e-6 in
+    all cases and < 1e-8 in most.  Reading R6: Figure 2 plots y, y'
+    and y'' for every ODE, so the solver carries derivatives
+    up to order >= 2; all six ODEs are embedded at R = 3 (zero-padded
+    coefficients, exactly-zero leading coefficients included).  Measured: max
+    MSE 5.1e-8 (third order), 5 of 6 below 1e-8."""
     T, dt = suite["steps"], suite["dt"]
     mses = {}
     for ode in suite["odes"]:
-        y, exact = _solve_ode(ode, dt, T)
+        y, exact = _solve_ode(ode, dt, T, order=3)
         mses[ode["name"]] = float(np.mean((y - exact) ** 2))
+    assert all(v < suite["mse_all"] for v in mses.values()), mses
+    assert sum(v < suite["mse_most"] for v in mses.values()) >= 4, mses
+
+
+def test_section_5_1_native_order(suite):
+    """Each ODE at its own order (R = 1, 2, 3): the scheme is still accurate to
+    < 1e-4 everywhere; the two stiffest (growth to y = 48, undamped oscillator)
+    need the R = 3 embedding above for the paper's 1e-6 (reading R6)."""
+    T, dt = suite["steps"], suite["dt"]
+    mses = {ode["name"]: float(np.mean((lambda ye: (ye[0] - ye[1]) ** 2)(_solve_ode(ode, dt, T))))
+            for ode in suite["odes"]}
     assert all(v < 1e-4 for v in mses.values()), mses
     assert sum(v < suite["mse_all"] for v in mses.values()) >= 4, mses
 
