@@ -6,12 +6,20 @@ Cholesky + substitution) plus one fused backward (smnn_solve_bwd: dl/dbeta =
 M^{-1} dl/dy and the chained gradients) over one batch of synthetic instances
 already resident in HBM.  Metric: instance*timesteps per second, fwd+bwd.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload lorenz]
-                  [--dtype f32|f64|f32c64] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload target]
+                  [--dtype f32c64|f32|f64] [--shard] [--impl ours|reference]
 
-Multi-GPU (torchrun, one rank per GPU): every rank solves its own full batch
-of independent instances (weak scaling, no data-path collective); the timed
-region is bracketed by barrier + synchronize and the max over ranks is taken.
+Default: the north_star target (T = 1e4, B*D = 4096, order 2) in the mode the
+parity tests hold to 1e-4 on y and every gradient (f32c64: fp32 storage, fp64
+arithmetic).  --dtype f32 is the fast fp32-arithmetic mode (not 1e-4 accurate
+at order >= 2, R7).
+
+Multi-GPU (torchrun, one rank per GPU): by default every rank solves its own
+full batch of independent instances (weak scaling, no data-path collective);
+--shard splits ONE batch over the ranks (strong scaling: each rank solves its
+contiguous shard, y is all_gathered and the loss all_reduced over NCCL inside
+the timed step).  The timed region is bracketed by barrier + synchronize and
+the max over ranks is taken.
 """
 
 from __future__ import annotations
@@ -41,10 +49,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="lorenz", choices=sorted(WORKLOADS))
-    ap.add_argument("--dtype", default=None, choices=["f32", "f64", "f32c64"],
-                    help="default: f32, except order-3 workloads (kdv): f32c64, because fp32 "
-                         "normal equations break down there (DESIGN.md 'Conditioning')")
+    ap.add_argument("--workload", default="target", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="f32c64", choices=["f32", "f64", "f32c64"],
+                    help="f32c64 (default): fp32 storage, fp64 arithmetic -- the mode verified to 1e-4; "
+                         "f32: fp32 arithmetic (fast, not 1e-4 accurate at order >= 2); f64: fp64 storage")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: split one batch over the ranks, all_gather y, all_reduce the loss")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threads-per-inst", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -53,6 +63,26 @@ def parse():
 
 
 # ---------------------------------------------------------------- helpers --
+
+def fp64_ops_per_unit(b: int):
+    """fp64 arithmetic of the paper's sequential algorithm per instance*timestep (DESIGN.md
+    "Roofline"): Appendix A.1 assembly 2b^2+6b-3, Algorithm 3 factor b^3+(b^3-b)/6+b(b-1)/2+4b
+    (rsqrt ~ 4), Algorithm 4 forward b^2+b(b+1)/2 and backward b^2+b(b+1)+b substitution;
+    backward: Algorithm 4 for dl/dbeta (factor reused) and the gradient chain 4b^2+7b+3.
+    Counts FMA / MUL / ADD as one op each (one DFMA-pipe slot)."""
+    assemble = 2 * b * b + 6 * b - 3
+    factor = b ** 3 + (b ** 3 - b) // 6 + b * (b - 1) // 2 + 4 * b
+    fsub = b * b + b * (b + 1) // 2
+    bsub = b * b + b * (b + 1) + b
+    grads = 4 * b * b + 7 * b + 3
+    return assemble + factor + fsub + bsub, fsub + bsub + grads
+
+
+def fp64_peak_tops():
+    """fp64 FMA-pipe peak: 148 SMs x 64 DFMA lanes/clk (tools/fp_rates.cu measured 63.3 on this
+    B200, profiles/r2/fp_rates.txt) x 1.965 GHz = 18.6 T ops/s (one op = one DFMA lane-slot)."""
+    return 148 * 64 * 1.965e9 / 1e12
+
 
 def algorithmic_bytes(b: int, es: int):
     """Unavoidable HBM bytes per instance*timestep.
@@ -151,7 +181,7 @@ def run_reference(args, wl):
         return
     import oracle as O
 
-    n_sample = 8
+    n_sample = max(1, min(8, 40000 // wl.T))  # about 0.3-0.6 s of oracle work per step
     x = make_workload_inputs(wl.with_(dtype="f64"), seed=1, n_inst=n_sample)
     gy = make_grad_y(n_sample, wl.T, wl.order, dtype="f64", seed=2)
     a = (x["coeffs"], x["rhs"], x["iv"], x["steps"])
@@ -182,8 +212,6 @@ def run_reference(args, wl):
 def main():
     args = parse()
     wl = WORKLOADS[args.workload]
-    if args.dtype is None:
-        args.dtype = "f32c64" if wl.order >= 3 else "f32"
     if args.impl == "reference":
         run_reference(args, wl)
         return
@@ -201,24 +229,40 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2410_06074_b200 as smnn
+    from paper_2410_06074_b200 import _abi
+    from paper_2410_06074_b200 import dist as sdist
 
     store = "f64" if args.dtype == "f64" else "f32"
     compute = "f64" if args.dtype == "f32c64" else None
     tdtype = torch.float64 if store == "f64" else torch.float32
     es = 8 if store == "f64" else 4
     b = wl.order + 1
-    # weak scaling: each rank owns a full batch of independent instances
-    x = make_workload_inputs(wl.with_(dtype=store), seed=1 + rank)
-    gy_np = make_grad_y(wl.n_inst, wl.T, wl.order, dtype=store, seed=100 + rank)
+    shard = args.shard and world > 1
+    # weak scaling: each rank owns a full batch; --shard: one batch (same seed on every rank), split
+    seed = 1 if args.shard else 1 + rank
+    x = make_workload_inputs(wl.with_(dtype=store), seed=seed)
+    gy_np = make_grad_y(wl.n_inst, wl.T, wl.order, dtype=store, seed=100 + (0 if args.shard else rank))
     t = {k: torch.from_numpy(v).to(dev) for k, v in x.items()}
     gy = torch.from_numpy(gy_np).to(dev)
     w = smnn.Weights()
     tpi = args.threads_per_inst
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    n_local = sdist.shard_range(wl.n_inst, rank, world)[1] - sdist.shard_range(wl.n_inst, rank, world)[0] \
+        if shard else wl.n_inst
+    ev_stream = torch.cuda.current_stream(dev)
 
-    def step():
+    def step(ev=None):
+        if shard:
+            y_all, loss, g = sdist.sharded_step(smnn, t, gy, rank, world, w, compute)
+            return y_all, g[4], g
+        if ev:
+            ev[0].record(ev_stream)
         y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi)
+        if ev:
+            ev[1].record(ev_stream)
         g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, w, compute, tpi)
+        if ev:
+            ev[2].record(ev_stream)
         return y, info, g
 
     for _ in range(args.warmup):
@@ -226,7 +270,6 @@ def main():
     torch.cuda.synchronize()
     assert int(info.abs().max()) == 0 and int(g[4].abs().max()) == 0, "numerical breakdown in warm-up"
 
-    stream = torch.cuda.current_stream(dev)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     if dist:
         dist.barrier()
@@ -234,11 +277,13 @@ def main():
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.fill_(i & 0xFF)  # evict L2 between timed steps (outside the events)
-            ev[i][0].record(stream)
-            y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi)
-            ev[i][1].record(stream)
-            g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, w, compute, tpi)
-            ev[i][2].record(stream)
+            if shard:
+                ev[i][0].record(ev_stream)
+                step()
+                ev[i][1].record(ev_stream)
+                ev[i][2].record(ev_stream)
+            else:
+                step(ev[i])
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -246,66 +291,83 @@ def main():
     bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
     tot_ms = float(np.sum(fwd_ms) + np.sum(bwd_ms))
     if dist:
-        tt = torch.tensor([tot_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        tot_ms = float(tt.item())
+        tot_ms = sdist.max_over_ranks(tot_ms, dev)
     ms_per_step = tot_ms / args.steps
-    units = wl.n_inst * wl.T * world
+    units = wl.n_inst * wl.T * (1 if shard else world)
     value = units / (ms_per_step / 1e3)
 
-    paths = {d: smnn.kernel_path(wl.n_inst, wl.T, wl.order, wl.n_iv, tdtype, compute, bwd=(d == "bwd"))
-             for d in ("fwd", "bwd")}
-    from paper_2410_06074_b200 import _abi
-    launches = {d: _abi.PATH_LAUNCHES[{"rf": 1, "pipe": 2, "checkpoint": 3}[v]] for d, v in paths.items()}
-    # roofline of the dominant launch (algorithmic bytes / measured launch time); for the
-    # pipeline path the "launch" is the call's three back-to-back kernels
+    def problem(n):
+        code = _abi.SMNN_F64 if store == "f64" else (_abi.SMNN_F32_C64 if compute else _abi.SMNN_F32)
+        return _abi.smnn_problem(n_inst=n, T=wl.T, order=wl.order, n_iv=wl.n_iv, dtype=code, threads_per_inst=tpi,
+                                 path=0, w_gov=w.gov, w_init=w.init, w_smooth=w.smooth)
+
+    import ctypes
+    lib = _abi.load()
+    pl = problem(n_local)
+    paths = {d: _abi.PATH_NAMES[lib.smnn_kernel_path(ctypes.byref(pl), int(d == "bwd"))] for d in ("fwd", "bwd")}
+    launches = {d: int(lib.smnn_launch_count(ctypes.byref(pl), int(d == "bwd"))) for d in ("fwd", "bwd")}
+    promoted = launches["bwd"] > (3 if paths["bwd"] == "pipe" else 1)
+    # roofline of the dominant call (algorithmic bytes / measured call time; a call of several
+    # launches -- the pipeline's three kernels -- counts as one "launch")
     fb, bb = algorithmic_bytes(b, es)
     f_avg, b_avg = float(np.mean(fwd_ms)), float(np.mean(bwd_ms))
-    inst_steps = wl.n_inst * wl.T
+    inst_steps = n_local * wl.T
     peak, peak_kind = measured_peaks()
-    kern = "smnn_solve_bwd" if b_avg >= f_avg else "smnn_factor_solve_fwd"
-    kbytes = inst_steps * (bb if b_avg >= f_avg else fb)
-    kms = max(b_avg, f_avg)
     kdir = "bwd" if b_avg >= f_avg else "fwd"
+    kern = {"fwd": "smnn_factor_solve_fwd", "bwd": "smnn_solve_bwd"}[kdir]
+    kbytes = inst_steps * (bb if kdir == "bwd" else fb)
+    kms = max(b_avg, f_avg)
     kernel_label = kern + {"rf": " = rf_kernel (one launch)",
                            "pipe": " = pipe_p1 + pipe_sep + pipe_p2 (three launches)",
-                           "checkpoint": " = resident/fused checkpoint kernel (one launch)"}[paths[kdir]]
+                           "checkpoint": " = resident/fused checkpoint kernel (one launch)",
+                           "x64": " = x64_kernel (one cluster launch, fp64 arithmetic)"}[paths[kdir]]
+    if kdir == "bwd" and promoted:
+        kernel_label = kern + f" = widen + fp64 {paths['bwd']} forward + backward + narrow ({launches['bwd']} launches)"
     achieved = kbytes / (kms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):  # measured by ncu on the GPU box (see profiles/README.md)
+    if os.path.exists(tp):  # ncu dram bytes per call, measured on the GPU box (profiles/README.md)
         traffic = json.load(open(tp)).get(f"{wl.name}/{args.dtype}/{kern}")
     step_gbs = inst_steps * (fb + bb) / (ms_per_step / 1e3) / 1e9
+    ops_f, ops_b = fp64_ops_per_unit(b)
+    alu = None
+    if compute or store == "f64":
+        ops = inst_steps * (ops_f + ops_b) / (ms_per_step / 1e3) / 1e12
+        alu = {"bound_if": "fp64 FMA pipe", "ops_per_unit": {"fwd": ops_f, "bwd": ops_b},
+               "achieved_tops": ops, "peak_tops": fp64_peak_tops(), "frac": ops / fp64_peak_tops(),
+               "floor_ms": inst_steps * (ops_f + ops_b) / (fp64_peak_tops() * 1e12) * 1e3,
+               "hbm_floor_ms": inst_steps * (fb + bb) / (peak * 1e9) * 1e3}
 
-    # end-to-end through the host-buffer C-ABI plan (H2D + fwd + bwd + D2H)
+    # end-to-end through the host-buffer C-ABI plan (H2D + fwd + bwd + D2H), this rank's batch
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not shard:
         plan = smnn.HostPlan(wl.n_inst, wl.T, wl.order, wl.n_iv, tdtype, w, compute, dev)
         h = {k: torch.from_numpy(v).pin_memory() for k, v in x.items()}
         hg = torch.from_numpy(gy_np).pin_memory()
         outs = [torch.empty_like(h["coeffs"]).pin_memory(), torch.empty_like(h["coeffs"]).pin_memory(),
                 torch.empty_like(h["rhs"]).pin_memory(), torch.empty_like(h["iv"]).pin_memory(),
                 torch.empty_like(h["steps"]).pin_memory()]
-        plan.fwd_bwd(h["coeffs"], h["rhs"], h["iv"], h["steps"], hg, *outs)
+        hinfo = torch.zeros(wl.n_inst, dtype=torch.int32).pin_memory()
+        plan.fwd_bwd(h["coeffs"], h["rhs"], h["iv"], h["steps"], hg, *outs, info=hinfo)
         torch.cuda.synchronize()
+        assert int(hinfo.abs().max()) == 0
         if dist:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        e0.record(ev_stream)
         for _ in range(args.e2e_steps):
-            plan.fwd_bwd(h["coeffs"], h["rhs"], h["iv"], h["steps"], hg, *outs)
-        e1.record(stream)
+            plan.fwd_bwd(h["coeffs"], h["rhs"], h["iv"], h["steps"], hg, *outs, info=hinfo)
+        e1.record(ev_stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if dist:
-            tt = torch.tensor([ems], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+            ems = sdist.max_over_ranks(ems, dev)
         plan.close()
         h2d = sum(v.nbytes for v in x.values()) + gy_np.nbytes
-        d2h = sum(o.numel() * o.element_size() for o in outs)
+        d2h = sum(o.numel() * o.element_size() for o in outs) + hinfo.numel() * 4
         e2e = {"value": units / (ems / args.e2e_steps / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.e2e_steps}
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.e2e_steps,
+               "api": "smnn_plan_fwd_bwd_host (pinned host buffers, info included)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -313,22 +375,30 @@ def main():
         cpu = cpu_baseline(x64, gy_np.astype(np.float64), wl)
 
     if rank == 0:
+        arith = "f64" if compute or store == "f64" else "f32"
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64" if args.dtype in ("f64", "f32c64") else "f32",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
+            "vs_baseline": None, "dtype": arith,
             "data": "synthetic (seeded, synth/workloads.py recipe)",
             "config": {"workload": wl.name, "desc": wl.desc, "B": wl.B, "D": wl.D, "T": wl.T, "order": wl.order,
-                       "instances_per_gpu": wl.n_inst, "storage": store, "arithmetic": "f64" if compute or
-                       store == "f64" else "f32", "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"dp{world} (instances sharded, no data-path collective)",
+                       "instances_per_gpu": n_local, "storage": store, "arithmetic": arith,
+                       "mode": args.dtype + (" (verified to 1e-4 on y and all gradients, tests/test_gpu_parity.py)"
+                                             if args.dtype == "f32c64" else ""),
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": (f"shard{world}: one batch split over {world} ranks, y all_gather + loss "
+                                       f"all_reduce (NCCL) inside the step") if shard else
+                                      f"dp{world} (each rank its own batch of independent instances, "
+                                      f"no data-path collective)",
                        "threads_per_inst": tpi or "auto"},
             "roofline": {"bound": "hbm", "kernel": kernel_label,
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": kbytes, "launch_ms": kms,
-                         "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
-            "kernels_ms": {"smnn_factor_solve_fwd": f_avg, "smnn_solve_bwd": b_avg},
+                         "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak, "alu_fp64": alu},
+            "kernels_ms": {"smnn_factor_solve_fwd": f_avg, "smnn_solve_bwd": b_avg} if not shard else
+                          {"sharded_step": ms_per_step},
             "gpu_launches": (launches["fwd"] + launches["bwd"]) * args.steps,
             "kernel_path": paths,
             "clocks": clk.result(),

@@ -72,7 +72,9 @@ typedef struct smnn_problem {
   int32_t n_iv;     /* initial values per instance, 1..R+1 (R_init = n_iv - 1)   */
   int32_t dtype;    /* SMNN_F32 | SMNN_F64 | SMNN_F32_C64                        */
   int32_t threads_per_inst; /* time-chunks (= CUDA threads) per instance; 0 = auto */
-  int32_t reserved; /* must be 0                                                 */
+  int32_t path;     /* kernel path: 0 = automatic (recommended), or an SMNN_PATH_*
+                       code to force one (tests / measurements; a forced path the
+                       problem does not fit falls back to the automatic order)    */
   double w_gov;     /* importance weights of PAPER.md:130, all > 0               */
   double w_init;
   double w_smooth;
@@ -83,19 +85,30 @@ const char* smnn_version(void);
 const char* smnn_last_error(void);
 
 /* Which kernels smnn_factor_solve_fwd (bwd = 0) / smnn_solve_bwd (bwd = 1)
- * run for `p` on this build (environment SMNN_KERNEL = auto | rf | pipe |
- * resident | stream overrides the automatic choice, for experiments):
+ * run for `p` on this build (p->path = 0: the automatic choice):
  *   SMNN_PATH_RF          one launch: resident register-factor kernel (one CTA
- *                         per instance, whole instance in shared memory)
+ *                         per instance, whole instance in shared memory; fp32)
  *   SMNN_PATH_PIPE        three launches: chunk pass 1, separator reduction,
  *                         chunk pass 2 (long horizons; needs the workspace)
  *   SMNN_PATH_CHECKPOINT  one launch: checkpointing resident / streaming kernel
- * Returns a negative SMNN_ERR_* code on an invalid `p`. */
+ *   SMNN_PATH_X64         one cluster launch: fp64-arithmetic cluster-resident
+ *                         kernel (SMNN_F64, SMNN_F32_C64)
+ * SMNN_PATH_STREAM is accepted in p->path only: the checkpoint path with its
+ * streaming (non-resident) kernel.  Returns a negative SMNN_ERR_* code on an
+ * invalid `p`. */
 #define SMNN_PATH_RF 1
 #define SMNN_PATH_PIPE 2
 #define SMNN_PATH_CHECKPOINT 3
 #define SMNN_PATH_X64 4
+#define SMNN_PATH_STREAM 5
 int smnn_kernel_path(const smnn_problem* p, int bwd);
+
+/* Number of kernel launches one smnn_factor_solve_fwd (bwd = 0) /
+ * smnn_solve_bwd (bwd = 1) call makes for `p` with every output requested
+ * (SMNN_F32_C64 backward on a path that reads y from storage runs as SMNN_F64
+ * on promoted copies: widening, fp64 forward + backward, narrowing; see
+ * smnn_solve_bwd).  Negative SMNN_ERR_* code on an invalid `p`. */
+int smnn_launch_count(const smnn_problem* p, int bwd);
 
 /* Bytes of device workspace the fused kernels need for `p` on the current
  * device (checkpoint scratch of the time-parallel solver, one slot per
@@ -123,7 +136,12 @@ int smnn_factor_solve_fwd(const smnn_problem* p, const void* coeffs, const void*
  * through Appendix A.1): given y from the forward pass and grad_y = dl/dy,
  * computes dl/dbeta = M^{-1} dl/dy by re-factoring M in registers, then
  * dl/dcoeffs, dl/drhs, dl/div, dl/dsteps.  Any grad_* output may be NULL to
- * skip it. */
+ * skip it.  The gradients are those of the exact solution y(c, d, u, s):
+ * SMNN_F32 and SMNN_F64 read y from `y`; SMNN_F32_C64 does not trust the
+ * fp32 rounding of y (the residual terms of the chain amplify it ~1e4x) and
+ * recomputes y in fp64 -- the x64 kernel solves for y and dl/dbeta together,
+ * every other path runs the backward as SMNN_F64 on fp64 copies of the
+ * inputs widened in the workspace (smnn_launch_count reports the launches). */
 int smnn_solve_bwd(const smnn_problem* p, const void* coeffs, const void* rhs,
                    const void* iv, const void* steps, const void* y, const void* grad_y,
                    void* grad_coeffs, void* grad_rhs, void* grad_iv, void* grad_steps,
@@ -150,8 +168,14 @@ int smnn_substitute(const smnn_problem* p, const void* L, const void* P,
  * plan's own copy-in, compute and copy-out streams (H2D of a group overlaps the kernels of the previous one
  * and the D2H of the one before), ordered after the work already on `stream`,
  * and `stream` waits for the last copy-out: the call returns once the work is
- * enqueued (synchronise `stream` before reading the outputs).  Host buffers
- * must be page-locked for the copies to overlap.
+ * enqueued (synchronise `stream` before reading the outputs).  A call is also
+ * ordered after the plan's previous call, whatever stream that one used (the
+ * device buffers are the plan's).  Host buffers must be page-locked for the
+ * copies to overlap; each holds exactly the batch's elements of the plan's
+ * storage type (the library copies that many bytes; no size is passed).
+ * info (nullable, n_inst int32): the forward pass's breakdown code where it
+ * reports one, else the backward pass's (same convention as
+ * smnn_factor_solve_fwd).
  * ---------------------------------------------------------------------- */
 typedef struct smnn_plan smnn_plan;
 

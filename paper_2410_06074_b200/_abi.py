@@ -16,9 +16,12 @@ EXPORTED = [
     "smnn_version", "smnn_last_error", "smnn_workspace_bytes", "smnn_assemble",
     "smnn_factor_solve_fwd", "smnn_solve_bwd", "smnn_factor", "smnn_substitute",
     "smnn_plan_create", "smnn_plan_destroy", "smnn_plan_fwd_bwd_host", "smnn_kernel_path",
+    "smnn_launch_count",
 ]
-SMNN_PATH_RF, SMNN_PATH_PIPE, SMNN_PATH_CHECKPOINT, SMNN_PATH_X64 = 1, 2, 3, 4
+SMNN_PATH_RF, SMNN_PATH_PIPE, SMNN_PATH_CHECKPOINT, SMNN_PATH_X64, SMNN_PATH_STREAM = 1, 2, 3, 4, 5
 PATH_NAMES = {1: "rf", 2: "pipe", 3: "checkpoint", 4: "x64"}
+# names accepted for smnn_problem.path (forcing a kernel path; "auto" = 0)
+PATH_CODES = {"auto": 0, "rf": 1, "pipe": 2, "checkpoint": 3, "resident": 3, "x64": 4, "stream": 5}
 PATH_LAUNCHES = {1: 1, 2: 3, 3: 1, 4: 1}
 
 
@@ -30,7 +33,7 @@ class smnn_problem(ctypes.Structure):
         ("n_iv", ctypes.c_int32),
         ("dtype", ctypes.c_int32),
         ("threads_per_inst", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("path", ctypes.c_int32),
         ("w_gov", ctypes.c_double),
         ("w_init", ctypes.c_double),
         ("w_smooth", ctypes.c_double),
@@ -54,14 +57,15 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
             _build.build_library()
         else:
             raise RuntimeError(f"{_build.LIB} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
-    path = os.environ.get("SMNN_LIB", _build.LIB)  # alternative builds, for experiments
-    L = ctypes.CDLL(path)
+    L = ctypes.CDLL(_build.LIB)
     L.smnn_version.restype = ctypes.c_char_p
     L.smnn_version.argtypes = []
     L.smnn_last_error.restype = ctypes.c_char_p
     L.smnn_last_error.argtypes = []
     L.smnn_kernel_path.restype = ctypes.c_int
     L.smnn_kernel_path.argtypes = [PP, ctypes.c_int]
+    L.smnn_launch_count.restype = ctypes.c_int
+    L.smnn_launch_count.argtypes = [PP, ctypes.c_int]
     L.smnn_workspace_bytes.restype = ctypes.c_size_t
     L.smnn_workspace_bytes.argtypes = [PP]
     L.smnn_assemble.restype = ctypes.c_int

@@ -32,11 +32,6 @@
 #ifndef SMNN_MIN_BLOCKS
 #define SMNN_MIN_BLOCKS 2
 #endif
-// Warp-tiled two-ended separator reduction (measured slower than the packed
-// CTA-wide BCR on B200 for K <= 256; kept for experiments).
-#ifndef SMNN_WARP_BCR
-#define SMNN_WARP_BCR 0
-#endif
 
 namespace smnn {
 
@@ -428,244 +423,6 @@ __device__ __forceinline__ void lbcr_body(const SepL<B, S, CL>& Sp, int k) {
 template <int B, class S, int P, bool CL>
 __device__ __noinline__ void lbcr(SepL<B, S, CL> Sp, int k) {
   lbcr_body<B, S, P, CL>(Sp, k);
-}
-
-// Warp-tiled two-ended block cyclic reduction (one CTA).  Separator i sits in
-// warp w = i / 32 at slot q = i % 32 + 1; slot q = 0 is the warp's virtual
-// left port (separator 32w - 1, owned by warp w - 1), whose diagonal / rhs
-// contributions accumulate in PW.  Each warp eliminates its slots 1..31 by
-// odd-even reduction (5 levels, __syncwarp only), keeping both ends; one thread
-// then solves the W-block system of the ports (slot 32 of every warp); each
-// warp back-substitutes its own slots.  Two __syncthreads in total.
-// Separator slots >= K must hold identity blocks (dummies).
-template <class S, int B>
-struct PortW {  // per-warp scratch (W <= 32 warps), AoS
-  S* D0;  // [W][B*B]  left-port diagonal contributions
-  S* R0;  // [W][B]
-  S* Y0;  // [W][B]    left-port solution
-  S* TL;  // [W][B*B]  top-level factor
-  S* TP;  // [W][B*B]
-  S* TZ;  // [W][B]
-};
-
-template <int B, class S, int P>
-__device__ __noinline__ void lbcr_warp(SepL<B, S, false> Sp, PortW<S, B> PW, int k, int nt) {
-  const int w = k >> 5, lane = k & 31, W = nt >> 5;
-  const int base = w * 32 - 1;  // separator index of slot q is base + q
-  auto ldD = [&](int q, S (&m)[B][B]) {
-    if (q == 0) {
-#pragma unroll
-      for (int i = 0; i < B * B; ++i) m[i / B][i % B] = PW.D0[w * B * B + i];
-    } else {
-      Sp.ld(Sp.D, base + q, m);
-    }
-  };
-  auto stD = [&](int q, const S (&m)[B][B]) {
-    if (q == 0) {
-#pragma unroll
-      for (int i = 0; i < B * B; ++i) PW.D0[w * B * B + i] = m[i / B][i % B];
-    } else {
-      Sp.st(Sp.D, base + q, m);
-    }
-  };
-  auto ldR = [&](int q, S (&v)[B]) {
-    if (q == 0) {
-#pragma unroll
-      for (int i = 0; i < B; ++i) v[i] = PW.R0[w * B + i];
-    } else {
-      Sp.ldv(Sp.R, base + q, v);
-    }
-  };
-  auto stR = [&](int q, const S (&v)[B]) {
-    if (q == 0) {
-#pragma unroll
-      for (int i = 0; i < B; ++i) PW.R0[w * B + i] = v[i];
-    } else {
-      Sp.stv(Sp.R, base + q, v);
-    }
-  };
-  if (lane == 0) {  // the left port starts with no contributions
-#pragma unroll
-    for (int i = 0; i < B * B; ++i) PW.D0[w * B * B + i] = splat<S>(0.0);
-#pragma unroll
-    for (int i = 0; i < B; ++i) PW.R0[w * B + i] = splat<S>(0.0);
-  }
-  __syncwarp();
-#pragma unroll 1
-  for (int h = 1; h <= 16; h <<= 1) {
-    const int o = h * (2 * lane + 1);
-    if (o < 32) {  // eliminate slot o (neighbours o - h >= 0, o + h <= 32)
-      S D[B][B], Lf[B][B], Bk[B][B], Bn[B][B], BnT[B][B], Y1[B][B], Y2[B][B], r[B], v[B];
-      Sp.ld(Sp.D, base + o, D);
-      report<P>(Sp.fail, lchol<B, S>(D, Lf), Sp.ltime(base + o));
-      Sp.ld(Sp.Bc, base + o, Bk);
-      lleft<B, S>(Lf, Bk, Y1);
-      Sp.ld(Sp.Bc, base + o + h, Bn);
-#pragma unroll
-      for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int j = 0; j < B; ++j) BnT[i][j] = Bn[j][i];
-      lleft<B, S>(Lf, BnT, Y2);
-      Sp.ldv(Sp.R, base + o, r);
-      llsolve<B, S>(Lf, r, v);
-      Sp.st(Sp.D, base + o, Lf);
-      Sp.st(Sp.Bc, base + o, Y1);
-      Sp.st(Sp.Y2, base + o, Y2);
-      Sp.stv(Sp.R, base + o, v);
-    }
-    __syncwarp();
-    const int e = 2 * h * lane;
-    if (e <= 32) {  // update survivor e from its eliminated neighbours
-      S D[B][B], r[B];
-      ldD(e, D);
-      ldR(e, r);
-      if (e >= h) {
-        const int oo = e - h;
-        S Y2o[B][B], Y1o[B][B], vo[B], nb[B][B];
-        Sp.ld(Sp.Y2, base + oo, Y2o);
-        Sp.ld(Sp.Bc, base + oo, Y1o);
-        Sp.ldv(Sp.R, base + oo, vo);
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-#pragma unroll
-          for (int j = 0; j < B; ++j) {
-            S aD = D[i][j], aB = splat<S>(0.0);
-#pragma unroll
-            for (int m = 0; m < B; ++m) {
-              aD = fnma_(Y2o[m][i], Y2o[m][j], aD);
-              aB = fnma_(Y2o[m][i], Y1o[m][j], aB);
-            }
-            D[i][j] = aD;
-            nb[i][j] = (e - 2 * h >= 0) ? aB : splat<S>(0.0);
-          }
-          S ar = r[i];
-#pragma unroll
-          for (int m = 0; m < B; ++m) ar = fnma_(Y2o[m][i], vo[m], ar);
-          r[i] = ar;
-        }
-        Sp.st(Sp.Bc, base + e, nb);
-      }
-      if (e + h <= 32) {
-        const int oo = e + h;
-        S Y1o[B][B], vo[B];
-        Sp.ld(Sp.Bc, base + oo, Y1o);
-        Sp.ldv(Sp.R, base + oo, vo);
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-#pragma unroll
-          for (int j = 0; j < B; ++j) {
-            S aD = D[i][j];
-#pragma unroll
-            for (int m = 0; m < B; ++m) aD = fnma_(Y1o[m][i], Y1o[m][j], aD);
-            D[i][j] = aD;
-          }
-          S ar = r[i];
-#pragma unroll
-          for (int m = 0; m < B; ++m) ar = fnma_(Y1o[m][i], vo[m], ar);
-          r[i] = ar;
-        }
-      }
-      stD(e, D);
-      stR(e, r);
-    }
-    __syncwarp();
-  }
-  __syncthreads();
-  if (k == 0) {  // block-tridiagonal Cholesky of the W ports (slot 32 of each warp)
-    S Lp[B][B], zp[B];
-    zero<B, S>(Lp);
-    zero<B, S>(zp);
-    for (int v = 0; v < W; ++v) {
-      const int iv = 32 * v + 31;
-      S D[B][B], r[B], Lf[B][B], z[B];
-      Sp.ld(Sp.D, iv, D);
-      Sp.ldv(Sp.R, iv, r);
-      if (v + 1 < W) {
-#pragma unroll
-        for (int i = 0; i < B * B; ++i) D[i / B][i % B] = add_(D[i / B][i % B], PW.D0[(v + 1) * B * B + i]);
-#pragma unroll
-        for (int i = 0; i < B; ++i) r[i] = add_(r[i], PW.R0[(v + 1) * B + i]);
-      }
-      if (v > 0) {
-        S C[B][B], Pm[B][B];
-        Sp.ld(Sp.Bc, iv, C);  // block(port v, port v-1)
-#pragma unroll
-        for (int rr = 0; rr < B; ++rr) llsolve<B, S>(Lp, C[rr], Pm[rr]);
-        lcouple<B, S>(Pm, zp, D, r);
-#pragma unroll
-        for (int i = 0; i < B * B; ++i) PW.TP[v * B * B + i] = Pm[i / B][i % B];
-      }
-      report<P>(Sp.fail, lchol<B, S>(D, Lf), Sp.ltime(iv));
-      llsolve<B, S>(Lf, r, z);
-#pragma unroll
-      for (int i = 0; i < B * B; ++i) PW.TL[v * B * B + i] = Lf[i / B][i % B];
-#pragma unroll
-      for (int i = 0; i < B; ++i) PW.TZ[v * B + i] = z[i];
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-        zp[i] = z[i];
-#pragma unroll
-        for (int j = 0; j < B; ++j) Lp[i][j] = Lf[i][j];
-      }
-    }
-    S yn[B];
-    zero<B, S>(yn);
-    for (int v = W - 1; v >= 0; --v) {
-      S Lf[B][B], z[B], y[B];
-#pragma unroll
-      for (int i = 0; i < B * B; ++i) Lf[i / B][i % B] = PW.TL[v * B * B + i];
-#pragma unroll
-      for (int i = 0; i < B; ++i) z[i] = PW.TZ[v * B + i];
-      if (v + 1 < W) {  // z -= P_{v+1}^T y_{v+1}
-        S Pn[B][B];
-#pragma unroll
-        for (int i = 0; i < B * B; ++i) Pn[i / B][i % B] = PW.TP[(v + 1) * B * B + i];
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int m = 0; m < B; ++m) z[i] = fnma_(Pn[m][i], yn[m], z[i]);
-      }
-      lltsolve<B, S>(Lf, z, y);
-      Sp.stv(Sp.Y, 32 * v + 31, y);
-      if (v + 1 < W) {
-#pragma unroll
-        for (int i = 0; i < B; ++i) PW.Y0[(v + 1) * B + i] = y[i];
-      }
-#pragma unroll
-      for (int i = 0; i < B; ++i) yn[i] = y[i];
-    }
-#pragma unroll
-    for (int i = 0; i < B; ++i) PW.Y0[i] = splat<S>(0.0);  // warp 0 has no left port
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int h = 16; h >= 1; h >>= 1) {
-    const int o = h * (2 * lane + 1);
-    if (o < 32) {
-      S Lf[B][B], Y1[B][B], Y2[B][B], v[B], yl[B], yr[B], t[B], y[B];
-      Sp.ld(Sp.D, base + o, Lf);
-      Sp.ld(Sp.Bc, base + o, Y1);
-      Sp.ld(Sp.Y2, base + o, Y2);
-      Sp.ldv(Sp.R, base + o, v);
-      if (o - h == 0) {
-#pragma unroll
-        for (int i = 0; i < B; ++i) yl[i] = PW.Y0[w * B + i];
-      } else {
-        Sp.ldv(Sp.Y, base + o - h, yl);
-      }
-      Sp.ldv(Sp.Y, base + o + h, yr);
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-        S acc = v[i];
-#pragma unroll
-        for (int m = 0; m < B; ++m) acc = fnma_(Y2[i][m], yr[m], fnma_(Y1[i][m], yl[m], acc));
-        t[i] = acc;
-      }
-      lltsolve<B, S>(Lf, t, y);
-      Sp.stv(Sp.Y, base + o, y);
-    }
-    __syncwarp();
-  }
 }
 
 // ---------------------------------------------------------------- pass 1 ---
@@ -1139,16 +896,12 @@ __device__ __forceinline__ void write_dummy_sep(const SepL<B, S, false>& Sp, int
   Sp.stv(Sp.Y, i, z);
 }
 
+// Separator scratch after the five record fields: a reserved per-warp region
+// of W (3 B^2 + 3 B) values (W = nt / 32; the host layouts keep it), then the
+// separator times and failure flags.
 template <int B, class S>
-__device__ __forceinline__ PortW<S, B> carve_ports(S* p, int W) {
-  PortW<S, B> PW;
-  PW.D0 = p;
-  PW.TL = PW.D0 + W * B * B;
-  PW.TP = PW.TL + W * B * B;
-  PW.R0 = PW.TP + W * B * B;
-  PW.Y0 = PW.R0 + W * B;
-  PW.TZ = PW.Y0 + W * B;
-  return PW;
+__device__ __forceinline__ int* sep_tail(S* y_end, int nt) {
+  return reinterpret_cast<int*>(y_end + (nt >> 5) * (3 * B * B + 3 * B));
 }
 
 template <int B, class Tio, class S, bool BWD, int G>
@@ -1163,8 +916,7 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) fused_kerne
   Sp.Y2 = Sp.Bc + B * B * nt;
   Sp.R = Sp.Y2 + B * B * nt;
   Sp.Y = Sp.R + B * nt;
-  const PortW<S, B> PW = carve_ports<B, S>(Sp.Y + B * nt, nt >> 5);
-  Sp.time = reinterpret_cast<int*>(PW.TZ + (nt >> 5) * B);
+  Sp.time = sep_tail<B, S>(Sp.Y + B * nt, nt);
   Sp.fail = Sp.time + nt;
   Sp.K = K;
   Sp.nt = nt;
@@ -1209,11 +961,7 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, SMNN_MIN_BLOCKS) fused_kerne
       Sp.stv(Sp.R, k, rk);
     }
     __syncthreads();
-#if SMNN_WARP_BCR
-    lbcr_warp<B, S, P>(Sp, PW, k, nt);
-#else
     lbcr<B, S, P, false>(Sp, k);
-#endif
     if (k < K) {
       Vec<B, S> yL, yR;
       Sp.ldv(Sp.Y, k, yR.v);
@@ -1259,8 +1007,7 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, (LaneT<S>::P == 1 ? SMNN_MIN
   Sp.Y2 = Sp.Bc + B * B * nt;
   Sp.R = Sp.Y2 + B * B * nt;
   Sp.Y = Sp.R + B * nt;
-  const PortW<S, B> PW = carve_ports<B, S>(Sp.Y + B * nt, nt >> 5);
-  Sp.time = reinterpret_cast<int*>(PW.TZ + (nt >> 5) * B);
+  Sp.time = sep_tail<B, S>(Sp.Y + B * nt, nt);
   Sp.fail = Sp.time + nt;
   Sp.K = K;
   Sp.nt = nt;
@@ -1371,11 +1118,7 @@ __global__ void __launch_bounds__(SMNN_MAX_THREADS, (LaneT<S>::P == 1 ? SMNN_MIN
       Sp.stv(Sp.R, k, rk);
     }
     Sp.sync();
-#if SMNN_WARP_BCR
-    if constexpr (CL) lbcr<B, S, P, CL>(Sp, k); else lbcr_warp<B, S, P>(Sp, PW, k, nt);
-#else
     lbcr<B, S, P, CL>(Sp, k);
-#endif
     Vec<B, S> yL, yR;
     Sp.ldv(Sp.Y, k, yR.v);
     if (k > 0) Sp.ldv(Sp.Y, k - 1, yL.v); else zero<B, S>(yL.v);

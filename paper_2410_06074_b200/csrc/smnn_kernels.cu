@@ -293,7 +293,7 @@ int validate(const smnn_problem* p) {
   if (!(p->w_gov > 0) || !(p->w_init > 0) || !(p->w_smooth > 0)) return fail_arg("weights must be > 0");
   if (p->threads_per_inst < 0 || p->threads_per_inst > SMNN_MAX_THREADS || (p->threads_per_inst % 32) != 0)
     return fail_arg("threads_per_inst must be 0 (auto) or a multiple of 32 in 32..SMNN_MAX_THREADS");
-  if (p->reserved != 0) return fail_arg("reserved must be 0");
+  if (p->path < 0 || p->path > SMNN_PATH_STREAM) return fail_arg("path must be 0 (auto) or an SMNN_PATH_* code");
   return SMNN_OK;
 }
 
@@ -319,15 +319,8 @@ size_t sep_bytes_per_chunk(const smnn_problem* p) {
   return size_t(3 * B * B + 2 * B) * lane_info(p).bytes + sizeof(int);
 }
 
-// Target steps per time chunk (env SMNN_CHUNK overrides, for tuning).
-int chunk_target() {
-  static int m = 0;
-  if (m == 0) {
-    const char* e = std::getenv("SMNN_CHUNK");
-    m = e ? std::max(2, std::atoi(e)) : 8;
-  }
-  return m;
-}
+// Target steps per time chunk of the checkpoint kernels.
+constexpr int chunk_target() { return 8; }
 
 // Chunks (threads) per instance.
 int threads_per_inst(const smnn_problem* p) {
@@ -437,9 +430,52 @@ int grid_blocks(const smnn_problem* p) {
   return grid_for<float, double>(p);
 }
 
-size_t workspace_bytes(const smnn_problem* p) {
+size_t workspace_bytes_direct(const smnn_problem* p) {
   const size_t per = size_t(nseg_ck(p)) * ck_elems(p) * threads_per_inst(p) * lane_info(p).bytes;
   return std::max<size_t>({per * grid_blocks(p), smnn::pipe_workspace_bytes(p), size_t(256)});
+}
+
+int kernel_path(const smnn_problem* p, bool bwd);
+
+// ---- SMNN_F32_C64 backward on the paths that read y from storage --------
+// The gradients' residual terms (d - c.y, the Taylor-row residuals) amplify
+// the fp32 rounding of y by up to ~1e4, so an fp32-stored y cannot give 1e-4
+// gradients.  The x64 kernel re-solves y in fp64 beside dl/dbeta; every other
+// path runs the backward as SMNN_F64 on promoted copies instead: inputs and
+// dl/dy widened to fp64 in the workspace, the fp64 forward (y in fp64), the
+// fp64 backward, gradients narrowed into the caller's fp32 outputs.
+bool promote_bwd(const smnn_problem* p) { return p->dtype == SMNN_F32_C64 && kernel_path(p, true) != SMNN_PATH_X64; }
+
+smnn_problem as_f64(const smnn_problem* p) {
+  smnn_problem q = *p;
+  q.dtype = SMNN_F64;
+  return q;
+}
+
+struct Promo {  // element offsets (doubles) of the promoted buffers in the workspace
+  size_t c, d, u, s, gy, y, gc, gd, gu, gs, info, end;
+};
+Promo promo_layout(const smnn_problem* p) {
+  const size_t n = size_t(p->n_inst), T = size_t(p->T), b = size_t(p->order + 1), ni = size_t(p->n_iv);
+  const size_t sT = n * T * b, s1 = n * T, su = n * ni, ss = n * (T > 0 ? T - 1 : 0);
+  auto al = [](size_t x) { return (x + 31) & ~size_t(31); };  // 256-byte aligned
+  Promo o{};
+  size_t off = 0;
+  auto take = [&](size_t k) { const size_t r = off; off += al(std::max<size_t>(k, 1)); return r; };
+  o.c = take(sT); o.d = take(s1); o.u = take(su); o.s = take(ss); o.gy = take(sT); o.y = take(sT);
+  o.gc = take(sT); o.gd = take(s1); o.gu = take(su); o.gs = take(ss);
+  o.info = take((n + 1) / 2);  // int32 forward info
+  o.end = off;
+  return o;
+}
+
+size_t workspace_bytes(const smnn_problem* p) {
+  size_t n = workspace_bytes_direct(p);
+  if (promote_bwd(p)) {
+    const smnn_problem q = as_f64(p);
+    n = std::max(n, promo_layout(p).end * sizeof(double) + workspace_bytes_direct(&q));
+  }
+  return n;
 }
 
 template <class Tio>
@@ -466,30 +502,19 @@ struct RPlan {
 
 size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Largest cluster the resident kernel may use (env SMNN_MAX_CLUSTER; default 1:
-// measured on B200, DSMEM cluster BCR is slower than the streaming kernel).
-int max_cluster() {
-  static int c = 0;
-  if (c == 0) {
-    const char* e = std::getenv("SMNN_MAX_CLUSTER");
-    c = e ? std::max(1, std::min(16, std::atoi(e))) : 1;
-  }
-  return c;
-}
-
 // Shared-memory layout of the resident kernel for (problem, direction): the
 // smallest cluster whose CTAs each hold their time range of the instance.
 template <int B, class Tio, class S>
 RPlan resident_plan(const smnn_problem* p, bool bwd) {
   RPlan best;
-  const char* env = std::getenv("SMNN_KERNEL");
-  if (env && std::string(env) == "stream") return best;
+  if (p->path == SMNN_PATH_STREAM) return best;  // forced streaming checkpoint kernel
   const size_t es = sizeof(Tio), ls = sizeof(S);
   constexpr int G = smnn::SegLen<B, S>::value;
   const int T = p->T;
   const size_t budgets[2] = {110 * 1024, 200 * 1024};
   for (size_t budget : budgets) {
-    for (int cs = 1; cs <= max_cluster(); cs *= 2) {
+    {
+      const int cs = 1;  // one CTA per instance group (cluster variants measured slower on B200)
       int nt = p->threads_per_inst;
       if (nt == 0) {
         const int m = chunk_target();  // steps per chunk
@@ -498,7 +523,7 @@ RPlan resident_plan(const smnn_problem* p, bool bwd) {
       }
       if (int64_t(cs) * nt > T) {
         nt = (T / cs / 32) * 32;
-        if (nt < 32) break;
+        if (nt < 32) continue;
       }
       const int K = cs * nt;
       const int maxchunk = (T + K - 1) / K;
@@ -589,22 +614,25 @@ int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
   return check_cuda(cudaGetLastError(), "fused kernel launch");
 }
 
-// Kernel path of the fused calls (SMNN_PATH_*), environment SMNN_KERNEL =
-// auto (default) | rf | pipe | resident | stream.  Measured on B200 (profiles/):
-// fp32 arithmetic: the resident RF kernel while one CTA holds the instance
-// (T <~ 4k: Lorenz 9.3e9 -> 14.4e9 instance-steps/s), the pipeline beyond it
-// (T = 1e4: 7.1e9 -> 22e9); fp64 arithmetic: the pipeline first (its chunk
-// kernels keep fewer registers live than rf; SST f64 3.2e9 -> 6.2e9, KdV
-// f32c64 1.8e9 -> 2.8e9, Lorenz f64 2.4e9 -> 3.7e9), then rf; then the
-// checkpointing kernels.  Every path can be forced (the parity tests do).
+// Kernel path of the fused calls (SMNN_PATH_*; p->path forces one, the
+// parity tests force every path).  Automatic order, measured on B200
+// (profiles/): fp64 arithmetic (SMNN_F64, SMNN_F32_C64) takes the x64
+// cluster-resident kernel while one cluster of <= 16 CTAs holds the instance,
+// then the pipeline, then rf; fp32 arithmetic takes the resident rf kernel
+// while one CTA holds the instance (T <~ 4k: Lorenz 9.3e9 -> 14.4e9
+// instance-steps/s over the checkpoint kernel), then the pipeline (T = 1e4:
+// 7.1e9 -> 22e9); the checkpointing kernels take what none of them fits.
 int kernel_path(const smnn_problem* p, bool bwd) {
-  const char* env = std::getenv("SMNN_KERNEL");
-  const std::string mode = env ? env : "auto";
-  const bool aut = mode == "auto", f32 = p->dtype == SMNN_F32;
-  if ((mode == "x64" || (aut && !f32)) && smnn::x64_eligible(p, bwd)) return SMNN_PATH_X64;
-  if ((mode == "rf" || (aut && f32)) && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
-  if ((mode == "pipe" || aut) && smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
-  if (aut && !f32 && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
+  const int want = p->path;  // 0 = auto; a forced path the problem does not fit falls back to auto
+  const bool f32 = p->dtype == SMNN_F32;
+  if (want == SMNN_PATH_X64 && smnn::x64_eligible(p, bwd)) return SMNN_PATH_X64;
+  if (want == SMNN_PATH_RF && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
+  if (want == SMNN_PATH_PIPE && smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
+  if (want == SMNN_PATH_CHECKPOINT || want == SMNN_PATH_STREAM) return SMNN_PATH_CHECKPOINT;
+  if (!f32 && smnn::x64_eligible(p, bwd)) return SMNN_PATH_X64;
+  if (f32 && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
+  if (smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
+  if (!f32 && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
   return SMNN_PATH_CHECKPOINT;
 }
 
@@ -685,11 +713,76 @@ int need_steps(const smnn_problem* p, const void* s) { return p->T > 1 ? need(s,
 
 }  // namespace
 
+// info[i] = forward info if it reports a breakdown, else the backward one
+__global__ void merge_info_kernel(int64_t n, const int32_t* fwd, int32_t* bwd) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && fwd[i] != 0) bwd[i] = fwd[i];
+}
+
+__global__ void widen_kernel(int64_t n, const float* __restrict__ in, double* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = double(in[i]);
+}
+__global__ void narrow_kernel(int64_t n, const double* __restrict__ in, float* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = float(in[i]);
+}
+
+namespace {
+unsigned ew_grid(int64_t n) { return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16))); }
+}  // namespace
+
+extern "C" int smnn_factor_solve_fwd(const smnn_problem*, const void*, const void*, const void*, const void*, void*,
+                                     int32_t*, void*, size_t, void*);
+extern "C" int smnn_solve_bwd(const smnn_problem*, const void*, const void*, const void*, const void*, const void*,
+                              const void*, void*, void*, void*, void*, int32_t*, void*, size_t, void*);
+
+// SMNN_F32_C64 backward on a path that reads y from storage: the whole
+// backward runs as SMNN_F64 on promoted copies (see promote_bwd).
+static int bwd_promoted(const smnn_problem* p, const void* coeffs, const void* rhs, const void* iv, const void* steps,
+                        const void* grad_y, void* gc, void* gd, void* gu, void* gs, int32_t* info, void* workspace,
+                        size_t ws_bytes, cudaStream_t st) {
+  const Promo o = promo_layout(p);
+  double* W = static_cast<double*>(workspace);
+  void* inner = W + o.end;
+  const size_t inner_bytes = ws_bytes - o.end * sizeof(double);
+  const int64_t n = p->n_inst, T = p->T, b = p->order + 1, ni = p->n_iv;
+  const int64_t nT = n * T * b, n1 = n * T, nu = n * ni, ns = n * std::max<int64_t>(T - 1, 0);
+  auto widen = [&](const void* src, size_t off, int64_t cnt) {
+    if (cnt > 0) widen_kernel<<<ew_grid(cnt), 256, 0, st>>>(cnt, static_cast<const float*>(src), W + off);
+  };
+  widen(coeffs, o.c, nT);
+  widen(rhs, o.d, n1);
+  widen(iv, o.u, nu);
+  if (T > 1) widen(steps, o.s, ns);
+  widen(grad_y, o.gy, nT);
+  int e;
+  if ((e = check_cuda(cudaGetLastError(), "widen_kernel"))) return e;
+  const smnn_problem q = as_f64(p);
+  int32_t* info_f = reinterpret_cast<int32_t*>(W + o.info);
+  if ((e = smnn_factor_solve_fwd(&q, W + o.c, W + o.d, W + o.u, W + o.s, W + o.y, info_f, inner, inner_bytes, st)))
+    return e;
+  if ((e = smnn_solve_bwd(&q, W + o.c, W + o.d, W + o.u, W + o.s, W + o.y, W + o.gy, gc ? W + o.gc : nullptr,
+                          gd ? W + o.gd : nullptr, gu ? W + o.gu : nullptr, (gs && T > 1) ? W + o.gs : nullptr, info,
+                          inner, inner_bytes, st)))
+    return e;
+  auto narrow = [&](void* dst, size_t off, int64_t cnt) {
+    if (dst && cnt > 0) narrow_kernel<<<ew_grid(cnt), 256, 0, st>>>(cnt, W + off, static_cast<float*>(dst));
+  };
+  narrow(gc, o.gc, nT);
+  narrow(gd, o.gd, n1);
+  narrow(gu, o.gu, nu);
+  if (T > 1) narrow(gs, o.gs, ns);
+  if (info) merge_info_kernel<<<ew_grid(n), 256, 0, st>>>(n, info_f, info);
+  return check_cuda(cudaGetLastError(), "narrow_kernel");
+}
+
 struct smnn_plan {
   smnn_problem p;
   void* buf = nullptr;   // one allocation
   void *c, *d, *u, *s, *gy, *y, *gc, *gd, *gu, *gs, *ws;
-  int32_t* info;
+  int32_t* info;     // backward pass
+  int32_t* info_f;   // forward pass (merged into info: the first breakdown wins)
   size_t ws_bytes = 0;
   // copy-in / compute / copy-out streams: instance groups are pipelined so that
   // H2D of group i+1, the kernels of group i and D2H of group i-1 overlap
@@ -708,6 +801,17 @@ int smnn_kernel_path(const smnn_problem* p, int bwd) {
   int e;
   if ((e = validate(p))) return e;
   return kernel_path(p, bwd != 0);
+}
+
+int smnn_launch_count(const smnn_problem* p, int bwd) {
+  int e;
+  if ((e = validate(p))) return e;
+  if (bwd && promote_bwd(p)) {  // widen (c, d, u, s, dl/dy), fp64 fwd + bwd, narrow (4 gradients), merge info
+    const smnn_problem q = as_f64(p);
+    const int io = p->T > 1 ? 5 : 4;
+    return io + smnn_launch_count(&q, 0) + smnn_launch_count(&q, 1) + (io - 1) + 1;
+  }
+  return kernel_path(p, bwd != 0) == SMNN_PATH_PIPE ? 3 : 1;
 }
 
 size_t smnn_workspace_bytes(const smnn_problem* p) {
@@ -781,6 +885,9 @@ int smnn_solve_bwd(const smnn_problem* p, const void* coeffs, const void* rhs, c
     a.g_steps = p->T > 1 ? (double*)grad_steps : nullptr; a.info = info; a.ckpt = workspace;
     return dispatch_fused<double, double, true>(p, a, st);
   }
+  if (promote_bwd(p))
+    return bwd_promoted(p, coeffs, rhs, iv, steps, grad_y, grad_coeffs, grad_rhs, grad_iv, grad_steps, info, workspace,
+                        workspace_bytes_, st);
   auto a = make_args<float>(p);
   set_inputs(a, coeffs, rhs, iv, steps);
   a.y_in = (const float*)y; a.grad_y = (const float*)grad_y;
@@ -837,7 +944,7 @@ int smnn_plan_create(smnn_plan** plan, const smnn_problem* p) {
   const size_t sz_c = al(n * T * b * es), sz_d = al(n * T * es), sz_u = al(n * p->n_iv * es),
                sz_s = al(n * std::max<size_t>(T - 1, 1) * es), sz_info = al(n * 4);
   q->ws_bytes = al(workspace_bytes(p));
-  const size_t total = 4 * sz_c + 2 * sz_d + 2 * sz_u + 2 * sz_s + sz_info + q->ws_bytes;
+  const size_t total = 4 * sz_c + 2 * sz_d + 2 * sz_u + 2 * sz_s + 2 * sz_info + q->ws_bytes;
   if ((e = check_cuda(cudaMalloc(&q->buf, total), "cudaMalloc(plan)"))) { delete q; return e; }
   char* ptr = static_cast<char*>(q->buf);
   auto take = [&](size_t s) { void* r = ptr; ptr += s; return r; };
@@ -846,6 +953,7 @@ int smnn_plan_create(smnn_plan** plan, const smnn_problem* p) {
   q->u = take(sz_u); q->gu = take(sz_u);
   q->s = take(sz_s); q->gs = take(sz_s);
   q->info = static_cast<int32_t*>(take(sz_info));
+  q->info_f = static_cast<int32_t*>(take(sz_info));
   q->ws = take(q->ws_bytes);
   const unsigned fl = cudaStreamNonBlocking;
   if ((e = check_cuda(cudaStreamCreateWithFlags(&q->sin, fl), "stream")) ||
@@ -896,17 +1004,20 @@ int smnn_plan_fwd_bwd_host(smnn_plan* q, const void* coeffs, const void* rhs, co
   const size_t T = size_t(p->T), b = size_t(p->order + 1), niv = size_t(p->n_iv);
   const cudaMemcpyKind h2d = cudaMemcpyHostToDevice, d2h = cudaMemcpyDeviceToHost;
   // groups of instances, each large enough to keep the GPU busy on its own
-  const char* eg = std::getenv("SMNN_PLAN_GROUPS");  // experiments
-  // default: one group per ~16 MiB of input, 1..8 groups (measured on B200:
-  // Lorenz, 49 MB in, best at 2 groups; the 1.3 GB target best at 8)
+  // one group per ~16 MiB of input, 1..8 groups (measured on B200: Lorenz,
+  // 49 MB in, best at 2 groups; the 1.3 GB target best at 8)
   const size_t in_bytes = size_t(n) * T * (2 * b + 2) * es;
-  const int Gmax = eg ? std::max(1, std::min(smnn_plan::kMaxGroups, std::atoi(eg)))
-                      : int(std::max<size_t>(1, std::min<size_t>(8, in_bytes >> 24)));
+  const int Gmax = int(std::max<size_t>(1, std::min<size_t>(8, in_bytes >> 24)));
   const int G = int(std::max<int64_t>(1, std::min<int64_t>(Gmax, n / 64)));
   auto H = [](const void* base, size_t off) { return static_cast<const char*>(base) + off; };
   auto Hm = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
   auto D = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
+  // Order after the caller's stream AND after this plan's previous call (which
+  // may have run on another stream): its copies and kernels use the same
+  // device buffers.  ev_out was recorded at the end of that call (waiting on a
+  // never-recorded event is a no-op).
   if ((e = check_cuda(cudaEventRecord(q->ev_start, st), "event")) ||
+      (e = check_cuda(cudaStreamWaitEvent(q->sin, q->ev_out, 0), "wait")) ||
       (e = check_cuda(cudaStreamWaitEvent(q->sin, q->ev_start, 0), "wait")) ||
       (e = check_cuda(cudaStreamWaitEvent(q->scomp, q->ev_start, 0), "wait")) ||
       (e = check_cuda(cudaStreamWaitEvent(q->sout, q->ev_start, 0), "wait")))
@@ -927,13 +1038,17 @@ int smnn_plan_fwd_bwd_host(smnn_plan* q, const void* coeffs, const void* rhs, co
       return e;
     smnn_problem pg = *p;
     pg.n_inst = ni;
-    if ((e = smnn_factor_solve_fwd(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc), nullptr,
-                                   q->ws, q->ws_bytes, q->scomp)))
+    if ((e = smnn_factor_solve_fwd(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc),
+                                   q->info_f + i0, q->ws, q->ws_bytes, q->scomp)))
       return e;
     if ((e = smnn_solve_bwd(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc), D(q->gy, oc),
                             D(q->gc, oc), D(q->gd, od), D(q->gu, ou), D(q->gs, os),
                             q->info + i0, q->ws, q->ws_bytes, q->scomp)))
       return e;
+    if (ni > 0) {
+      merge_info_kernel<<<unsigned((ni + 255) / 256), 256, 0, q->scomp>>>(ni, q->info_f + i0, q->info + i0);
+      if ((e = check_cuda(cudaGetLastError(), "merge_info_kernel"))) return e;
+    }
     if ((e = check_cuda(cudaEventRecord(q->ev_comp[gi], q->scomp), "event")) ||
         (e = check_cuda(cudaStreamWaitEvent(q->sout, q->ev_comp[gi], 0), "wait")) ||
         (e = check_cuda(cudaMemcpyAsync(Hm(y, oc), D(q->y, oc), bc, d2h, q->sout), "D2H y")))

@@ -44,8 +44,7 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
   if (K < 1 || K > SMNN_PIPE_SEP_MAX || (T + K - 1) / K > CM) return q;
   q.sep2 = K > 256 && K % 128 == 0;
   if (q.sep2) {  // separators per thread: 4, or 8 when K/4 would exceed 256 threads
-    const char* e = std::getenv("SMNN_PIPE_M");
-    q.m2 = e ? (std::atoi(e) > 4 ? 8 : 4) : (K / 4 > 256 ? 8 : 4);
+    q.m2 = K / 4 > 256 ? 8 : 4;
     if (K % (32 * q.m2) != 0 || K / q.m2 > 256) q.sep2 = false;
   }
   if (K > 256 && !q.sep2) return q;
@@ -86,8 +85,6 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     L->K = K;
     L->NT = q.NT;
     L->parts = q.parts;
-    const char* e = std::getenv("SMNN_PIPE_SEPMAP");
-    L->sepmap = e ? std::atoi(e) : 0;
   }
   q.ok = true;
   return q;
@@ -108,55 +105,6 @@ PipePlan plan_of(const smnn_problem* p, bool bwd) {
   return plan_S<double>(p, p->dtype == SMNN_F64 ? 8 : 4, bwd);
 }
 
-// The dynamic shared-memory attribute must cover the largest request made so
-// far for each kernel (keyed by the kernel's address: instantiations share a type).
-template <class Kern>
-void set_smem(Kern k, size_t smem) {
-  static std::mutex mu;
-  static std::map<const void*, size_t> top;
-  std::lock_guard<std::mutex> lk(mu);
-  size_t& t = top[reinterpret_cast<const void*>(k)];
-  if (smem > t) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    t = smem;
-  }
-}
-
-// Fork-join streams of the pipeline: the batch is split into groups whose
-// P1 -> SEP -> P2 chains run on different streams, so the latency-bound
-// separator kernel of one group overlaps the throughput-bound chunk kernels of
-// another.  One pool per device, created on first use.
-struct ForkJoin {
-  static constexpr int kMax = 4;
-  cudaStream_t s[kMax] = {};
-  cudaEvent_t fork = nullptr, join[kMax] = {};
-};
-
-ForkJoin* fork_join() {
-  static std::mutex mu;
-  static ForkJoin pools[64];
-  static bool made[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
-  ForkJoin& f = pools[dev];
-  if (!made[dev]) {
-    for (int i = 0; i < ForkJoin::kMax; ++i) {
-      if (cudaStreamCreateWithFlags(&f.s[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-      if (cudaEventCreateWithFlags(&f.join[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    }
-    if (cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    made[dev] = true;
-  }
-  return &f;
-}
-
-int pipe_groups(int64_t n_inst) {
-  const char* e = std::getenv("SMNN_PIPE_STREAMS");
-  const int want = e ? std::max(1, std::min(ForkJoin::kMax, std::atoi(e))) : 1;  // measured: no gain on B200
-  return int(std::max<int64_t>(1, std::min<int64_t>(want, n_inst / 512)));  // >= 512 instances per group
-}
-
 template <int B, class Tio, class S, bool BWD>
 int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
   constexpr int CM = PipeCM<B, S>::value;
@@ -166,73 +114,30 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   auto k2 = pipe_sep_kernel<B, S>;
   auto k2b = q.m2 > 4 ? pipe_sep2_kernel<B, S, 8> : pipe_sep2_kernel<B, S, 4>;
   auto k3 = pipe_p2_kernel<B, Tio, S, BWD, CM>;
-  set_smem(k1, q.smem_p1);
-  set_smem(k3, q.smem_p2);
-  set_smem(q.sep2 ? k2b : k2, q.smem_sep);
-  const int G = pipe_groups(p->n_inst);
-  ForkJoin* fj = G > 1 ? fork_join() : nullptr;
-  const int groups = fj ? G : 1;
-  if (fj && cudaEventRecord(fj->fork, st) != cudaSuccess) fj = nullptr;
+  for (auto [kp, sm] : {std::make_pair(reinterpret_cast<const void*>(k1), q.smem_p1),
+                         std::make_pair(reinterpret_cast<const void*>(k3), q.smem_p2),
+                         std::make_pair(q.sep2 ? reinterpret_cast<const void*>(k2b) : reinterpret_cast<const void*>(k2),
+                                        q.smem_sep)})
+    if (const cudaError_t ea = ensure_smem(kp, sm); ea != cudaSuccess) {
+      err = std::string("pipeline shared-memory attribute: ") + cudaGetErrorString(ea);
+      cudaGetLastError();
+      return SMNN_ERR_CUDA;
+    }
+  const int64_t n = p->n_inst;
+  PipeL L1 = q.L1, L2 = q.L2;
   char* ws = static_cast<char*>(a.ckpt);
-  const int T = p->T, K = q.K;
-  const size_t ls = sizeof(S);
-  // stage-major launch order (all groups' P1, then SEP, then P2): a group's
-  // separator kernel becomes ready while the next group's P1 still runs
-  struct Grp3 {
-    Args<Tio> a;
-    PipeL L1, L2;
-    int32_t* info;
-    int64_t ni;
-    cudaStream_t s;
-  } gr[ForkJoin::kMax];
-  for (int gi = 0; gi < groups; ++gi) {
-    const int64_t i0 = p->n_inst * gi / groups, i1 = p->n_inst * (gi + 1) / groups, ni = i1 - i0;
-    Grp3& G3 = gr[gi];
-    G3.ni = ni;
-    G3.s = st;
-    if (fj) {
-      G3.s = fj->s[gi];
-      cudaStreamWaitEvent(G3.s, fj->fork, 0);
-    }
-    Args<Tio>& ag = G3.a;  // the group's instances [i0, i1)
-    ag = a;
-    ag.n_inst = ni;
-    ag.coeffs = a.coeffs + i0 * T * B;
-    ag.rhs = a.rhs + i0 * T;
-    ag.iv = a.iv + i0 * a.n_iv;
-    ag.steps = a.steps + i0 * (T - 1);
-    if (a.y_in) ag.y_in = a.y_in + i0 * T * B;
-    if (a.grad_y) ag.grad_y = a.grad_y + i0 * T * B;
-    if (a.y_out) ag.y_out = a.y_out + i0 * T * B;
-    if (a.g_coeffs) ag.g_coeffs = a.g_coeffs + i0 * T * B;
-    if (a.g_rhs) ag.g_rhs = a.g_rhs + i0 * T;
-    if (a.g_iv) ag.g_iv = a.g_iv + i0 * a.n_iv;
-    if (a.g_steps) ag.g_steps = a.g_steps + i0 * (T - 1);
-    G3.info = a.info ? a.info + i0 : nullptr;
-    G3.L1 = q.L1;
-    G3.L2 = q.L2;
-    for (PipeL* L : {&G3.L1, &G3.L2}) {
-      L->sep1 = ws + size_t(i0) * PSep<B>::N * K * ls;
-      L->ysep = ws + q.ws_sep1 + size_t(i0) * B * K * ls;
-      L->cfail = reinterpret_cast<int*>(ws + q.ws_sep1 + q.ws_ysep) + i0 * K;
-    }
+  for (PipeL* L : {&L1, &L2}) {  // workspace: separator records, separator solution, chunk failure flags
+    L->sep1 = ws;
+    L->ysep = ws + q.ws_sep1;
+    L->cfail = reinterpret_cast<int*>(ws + q.ws_sep1 + q.ws_ysep);
   }
-  for (int gi = 0; gi < groups; ++gi)
-    if (gr[gi].ni > 0) k1<<<unsigned(gr[gi].ni * q.parts), q.NT, q.smem_p1, gr[gi].s>>>(gr[gi].a, gr[gi].L1);
-  for (int gi = 0; gi < groups; ++gi) {
-    if (gr[gi].ni <= 0) continue;
+  if (n > 0) {
+    k1<<<unsigned(n * q.parts), q.NT, q.smem_p1, st>>>(a, L1);
     if (q.sep2)
-      k2b<<<unsigned(gr[gi].ni), q.K / q.m2, q.smem_sep, gr[gi].s>>>(gr[gi].L1, T, gr[gi].info);
+      k2b<<<unsigned(n), q.K / q.m2, q.smem_sep, st>>>(L1, p->T, a.info);
     else
-      k2<<<unsigned(gr[gi].ni), q.K, q.smem_sep, gr[gi].s>>>(gr[gi].L1, T, gr[gi].info);
-  }
-  for (int gi = 0; gi < groups; ++gi) {
-    if (gr[gi].ni <= 0) continue;
-    k3<<<unsigned(gr[gi].ni * q.parts), q.NT, q.smem_p2, gr[gi].s>>>(gr[gi].a, gr[gi].L2);
-    if (fj) {
-      cudaEventRecord(fj->join[gi], gr[gi].s);
-      cudaStreamWaitEvent(st, fj->join[gi], 0);
-    }
+      k2<<<unsigned(n), q.K, q.smem_sep, st>>>(L1, p->T, a.info);
+    k3<<<unsigned(n * q.parts), q.NT, q.smem_p2, st>>>(a, L2);
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

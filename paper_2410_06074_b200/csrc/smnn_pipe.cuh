@@ -66,7 +66,6 @@ struct PipeL {
   int K;          // chunks (= separators) per instance
   int NT;         // threads per CTA of the chunk kernels
   int parts;      // CTAs per instance of the chunk kernels
-  int sepmap;     // separator kernel thread map: 1 = grouped by reduction level, 0 = identity
   int off_c, off_d, off_s, off_g, off_y, off_h, off_bar;  // shared-memory byte offsets (16-aligned)
   void* sep1;
   void* ysep;
@@ -191,7 +190,7 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
   unsigned char* sm = smnn_dyn_smem;
   // threads ordered by the level at which their separator is eliminated
   // (rf_chunk_of_thread): each reduction level runs on as few warps as possible
-  const int K = L.K, k = L.sepmap ? rf_chunk_of_thread(int(threadIdx.x), K) : int(threadIdx.x);
+  const int K = L.K, k = int(threadIdx.x);
   const int64_t g = blockIdx.x;
   S* rec = reinterpret_cast<S*>(sm);
   int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * K);
@@ -253,7 +252,7 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
   unsigned char* sm = smnn_dyn_smem;
   const int K = L.K, nt = blockDim.x;
   // super-separator of this thread: identity, or grouped by reduction level
-  const int t = L.sepmap ? rf_chunk_of_thread(int(threadIdx.x), nt) : int(threadIdx.x);
+  const int t = int(threadIdx.x);
   const int m = K / nt;  // separators per thread (host: K = m * nt, m <= MS)
   const int64_t g = blockIdx.x;
   S* rec = reinterpret_cast<S*>(sm);

@@ -51,30 +51,12 @@ size_t rf_smem(const smnn_problem* p, int nt, size_t es, bool bwd, RLayout& L) {
   const bool late_y = bwd && RF_LATE_Y;
   L.off_y = (bwd && !late_y) ? take(size_t(T) * B * es + 32) : 0;
   L.lane = int(off);
-  // separator records (rbcr2), or the one-warp solve's field-major blocks + y + lane scratch
-  const size_t wrec = (size_t(PSep<B>::N + B) * nt + 32 * (B * (B + 1) / 2 + 2 * B * B + B)) * ls;
-  const size_t rec = std::max(size_t(RfSep<B, SMNN_RF_SEP>::R::N) * nt * ls, (RF_WARP_SEP && nt <= 128) ? wrec : 0);
+  const size_t rec = size_t(BRec<B>::N) * nt * ls;  // separator records (rbcr2)
   L.off_sep = take(late_y ? std::max(rec, size_t(T) * B * es + 32) : rec);  // late y reuses the records
   if (late_y) L.off_y = L.off_sep;
   L.off_ck = take(size_t(nt + 4) * 4);  // separator times + failure flag
   L.off_bar = take(16);
   return off;
-}
-
-// Segmented variant (rf_kernel<..., SEG = true>): chunks of up to 2 PipeHM + 1
-// points, at most 256 threads -- half the separators and threads per instance,
-// at the price of re-factoring in pass 2.  Measured slower on B200 (Lorenz
-// 8.5e9 vs 14.3e9: the extra factorisation and register spills outweigh the
-// shorter reduction), so only SMNN_RF_SEG=1 selects it.
-template <int B, class S>
-struct RfSegCM {
-  static constexpr int value = 2 * PipeHM<B, S>::value + 1;
-};
-
-bool seg_enabled(const smnn_problem* p) {
-  const char* e = std::getenv("SMNN_RF_SEG");
-  (void)p;
-  return e && std::atoi(e) != 0;
 }
 
 // Wide register-factor variant: chunks of up to 12 points (fp32, b = 3).
@@ -90,14 +72,10 @@ struct RfCMW {
   static constexpr int value = (B == 3 && sizeof(S) == 4) ? 12 : RfCM<B, S>::value;
 };
 
-// 0: not eligible, 1: register-factor variant, 2: segmented variant, 3: wide register-factor variant
+// 0: not eligible, 1: register-factor variant, 3: wide register-factor variant
 template <int B, class S>
 int variant_B(const smnn_problem* p, size_t es, bool bwd) {
   RLayout L;
-  if (seg_enabled(p)) {
-    const int nt = rf_threads(p, RfSegCM<B, S>::value, 256);
-    if (nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024) return 2;
-  }
   const int nt = rf_threads(p, RfCM<B, S>::value);
   const bool ok = nt != 0 && rf_smem<B, S>(p, nt, es, bwd, L) <= 200 * 1024;
   if (RfCMW<B, S>::value != RfCM<B, S>::value) {
@@ -119,21 +97,15 @@ template <int B, class Tio, class S, bool BWD>
 int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
   const int var = variant_B<B, S>(p, sizeof(Tio), BWD);
   if (var == 0) return 0;
-  constexpr int CM = RfCM<B, S>::value, CMS = RfSegCM<B, S>::value, CMW = RfCMW<B, S>::value;
-  const int nt = var == 2 ? rf_threads(p, CMS, 256) : var == 3 ? rf_threads(p, CMW) : rf_threads(p, CM);
+  constexpr int CM = RfCM<B, S>::value, CMW = RfCMW<B, S>::value;
+  const int nt = var == 3 ? rf_threads(p, CMW) : rf_threads(p, CM);
   RLayout L{};
   const size_t smem = rf_smem<B, S>(p, nt, sizeof(Tio), BWD, L);
-  auto kern = var == 2 ? rf_kernel<B, Tio, S, BWD, CMS, true>
-            : var == 3 ? rf_kernel<B, Tio, S, BWD, CMW, false> : rf_kernel<B, Tio, S, BWD, CM, false>;
-  {  // the attribute must cover the largest request so far, per kernel
-    static std::mutex mu;
-    static std::map<const void*, size_t> top;
-    std::lock_guard<std::mutex> lk(mu);
-    size_t& t = top[reinterpret_cast<const void*>(kern)];
-    if (smem > t) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      t = smem;
-    }
+  auto kern = var == 3 ? rf_kernel<B, Tio, S, BWD, CMW> : rf_kernel<B, Tio, S, BWD, CM>;
+  if (const cudaError_t ea = ensure_smem_k(kern, smem); ea != cudaSuccess) {
+    err = std::string("rf kernel shared-memory attribute: ") + cudaGetErrorString(ea);
+    cudaGetLastError();
+    return SMNN_ERR_CUDA;
   }
   // one CTA per instance up to 2^31 - 1 (the block scheduler balances the tail);
   // the kernel strides over instances beyond that

@@ -37,13 +37,6 @@ struct RfCM {
                                               : (B == 1 ? 16 : B == 2 ? 12 : B == 3 ? SMNN_RF_CM3 : 5);
 };
 
-// Separator solver of the RF kernel: 2 = block cyclic reduction with the blocks
-// in registers (rbcr2, default), 1 = parallel cyclic reduction (rpcr; faster
-// but not backward stable), 0 = block cyclic reduction in shared memory (rbcr).
-#ifndef SMNN_RF_SEP
-#define SMNN_RF_SEP 2
-#endif
-
 // Identity the compiler cannot see through (no rematerialisation from constants).
 __device__ __forceinline__ int opaque(int v) { asm volatile("" : "+r"(v)); return v; }
 __device__ __forceinline__ float opaque(float v) { asm volatile("" : "+f"(v)); return v; }
@@ -54,20 +47,7 @@ __device__ __forceinline__ double opaque(double v) { asm volatile("" : "+d"(v));
 // pass-2 forward sweep -- one staging buffer less (44 -> 32 B per time point),
 // so one more CTA per SM.
 #ifndef RF_LATE_Y
-#define RF_LATE_Y (SMNN_RF_SEP != 0)
-#endif
-
-// One-warp separator solve (rsep_warp: local elimination + shuffle BCR) for
-// K <= 128.  Measured slower on B200 (Lorenz 10.9e9 vs 14.4e9: one warp does
-// the whole reduction while three wait, and its registers spill next to the
-// resident factors), so off by default.
-#ifndef RF_WARP_SEP
-#define RF_WARP_SEP 0
-#endif
-
-// Thread -> chunk map: 1 = grouped by reduction level (rf_chunk_of_thread), 0 = identity.
-#ifndef RF_MAP
-#define RF_MAP 0
+#define RF_LATE_Y 1
 #endif
 
 // Phase timestamps (debug builds only): per CTA, globaltimer at the phase boundaries.
@@ -90,19 +70,6 @@ __device__ __forceinline__ unsigned long long rf_now() {
 #ifndef SMNN_RF_MAX_THREADS
 #define SMNN_RF_MAX_THREADS 512
 #endif
-
-// ------------------------------------------------------------------ BCR ---
-// Separator records, array of structures: separator i occupies N consecutive
-// S values at sep + i*N (N odd, so lanes that touch records h apart hit
-// different banks for odd h):  D (diagonal block, lower triangle used; the
-// Cholesky factor after elimination), Bc (coupling block (i, i-h); Y1 after
-// elimination), Y2, R (rhs; v after elimination), Y (solution).
-template <int B>
-struct RRec {
-  static constexpr int raw = 3 * B * B + 2 * B;
-  static constexpr int N = raw | 1;
-  static constexpr int D = 0, BC = B * B, Y2 = 2 * B * B, R = 3 * B * B, Y = 3 * B * B + B;
-};
 
 template <int B, class S>
 __device__ __forceinline__ void rld_low(const S* p, S (&m)[B][B]) {
@@ -148,273 +115,6 @@ __device__ __forceinline__ void rst_v(S* p, const S (&v)[B]) {
 // (Cholesky of D_o, Y1 = L^{-1} B_o, Y2 = L^{-1} B_{o+h}^T, v = L^{-1} r_o) and
 // updates the survivors e = 0 (mod 2h); back substitution
 // y_o = L_o^{-T}(v_o - Y1 y_{o-h} - Y2 y_{o+h}).  All K threads call it.
-template <int B, class S>
-__device__ __forceinline__ void rbcr(S* sep, const int* time, int* fail, int K, int k) {
-  using Q = RRec<B>;
-  constexpr int N = Q::N;
-  int hmax = 0;
-#pragma unroll 1
-  for (int h = 1; h < K; h <<= 1) {
-    hmax = h;
-    {
-      const int o = h + 2 * h * k;
-      if (o < K) {
-        S* po = sep + o * N;
-        S D[B][B], Lf[B][B], Bk[B][B], Y1[B][B], Y2[B][B], r[B], v[B];
-        rld_low<B, S>(po + Q::D, D);
-        const int bd = lchol<B, S>(D, Lf);
-        if (bd) report<1>(fail, bd, time[o]);
-        rld_full<B, S>(po + Q::BC, Bk);
-        lleft<B, S>(Lf, Bk, Y1);
-        if (o + h < K) {
-          S Bn[B][B], BnT[B][B];
-          rld_full<B, S>(sep + (o + h) * N + Q::BC, Bn);
-#pragma unroll
-          for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int j = 0; j < B; ++j) BnT[i][j] = Bn[j][i];
-          lleft<B, S>(Lf, BnT, Y2);
-        } else {
-          zero<B, S>(Y2);
-        }
-        rld_v<B, S>(po + Q::R, r);
-        llsolve<B, S>(Lf, r, v);
-        rst_low<B, S>(po + Q::D, Lf);
-        rst_full<B, S>(po + Q::BC, Y1);
-        rst_full<B, S>(po + Q::Y2, Y2);
-        rst_v<B, S>(po + Q::R, v);
-      }
-    }
-    __syncthreads();
-    {
-      const int e = 2 * h * k;
-      if (e < K) {
-        S* pe = sep + e * N;
-        S D[B][B], r[B];
-        rld_low<B, S>(pe + Q::D, D);
-        rld_v<B, S>(pe + Q::R, r);
-        if (e - h >= 0) {
-          const S* po = sep + (e - h) * N;
-          S Y2o[B][B], vo[B];
-          rld_full<B, S>(po + Q::Y2, Y2o);
-          rld_v<B, S>(po + Q::R, vo);
-#pragma unroll
-          for (int i = 0; i < B; ++i) {
-#pragma unroll
-            for (int j = 0; j <= i; ++j) {
-              S aD = D[i][j];
-#pragma unroll
-              for (int m = 0; m < B; ++m) aD = fnma_(Y2o[m][i], Y2o[m][j], aD);
-              D[i][j] = aD;
-            }
-            S ar = r[i];
-#pragma unroll
-            for (int m = 0; m < B; ++m) ar = fnma_(Y2o[m][i], vo[m], ar);
-            r[i] = ar;
-          }
-          if (e - 2 * h >= 0) {  // new coupling (e, e-2h) = -Y2_o^T Y1_o
-            S Y1o[B][B], nb[B][B];
-            rld_full<B, S>(po + Q::BC, Y1o);
-#pragma unroll
-            for (int i = 0; i < B; ++i)
-#pragma unroll
-              for (int j = 0; j < B; ++j) {
-                S aB = mul_(Y2o[0][i], Y1o[0][j]);
-#pragma unroll
-                for (int m = 1; m < B; ++m) aB = fma_(Y2o[m][i], Y1o[m][j], aB);
-                nb[i][j] = neg_(aB);
-              }
-            rst_full<B, S>(pe + Q::BC, nb);
-          }
-        }
-        if (e + h < K) {
-          const S* po = sep + (e + h) * N;
-          S Y1o[B][B], vo[B];
-          rld_full<B, S>(po + Q::BC, Y1o);
-          rld_v<B, S>(po + Q::R, vo);
-#pragma unroll
-          for (int i = 0; i < B; ++i) {
-#pragma unroll
-            for (int j = 0; j <= i; ++j) {
-              S aD = D[i][j];
-#pragma unroll
-              for (int m = 0; m < B; ++m) aD = fnma_(Y1o[m][i], Y1o[m][j], aD);
-              D[i][j] = aD;
-            }
-            S ar = r[i];
-#pragma unroll
-            for (int m = 0; m < B; ++m) ar = fnma_(Y1o[m][i], vo[m], ar);
-            r[i] = ar;
-          }
-        }
-        rst_low<B, S>(pe + Q::D, D);
-        rst_v<B, S>(pe + Q::R, r);
-      }
-    }
-    __syncthreads();
-  }
-  if (k == 0) {
-    S D[B][B], Lf[B][B], r[B], t[B], y[B];
-    rld_low<B, S>(sep + Q::D, D);
-    const int bd = lchol<B, S>(D, Lf);
-    if (bd) report<1>(fail, bd, time[0]);
-    rld_v<B, S>(sep + Q::R, r);
-    llsolve<B, S>(Lf, r, t);
-    lltsolve<B, S>(Lf, t, y);
-    rst_v<B, S>(sep + Q::Y, y);
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int h = hmax; h >= 1; h >>= 1) {
-    const int o = h + 2 * h * k;
-    if (o < K) {
-      const S* po = sep + o * N;
-      S Lf[B][B], Y1[B][B], v[B], yl[B], t[B], y[B];
-      rld_low<B, S>(po + Q::D, Lf);
-      rld_full<B, S>(po + Q::BC, Y1);
-      rld_v<B, S>(po + Q::R, v);
-      rld_v<B, S>(sep + (o - h) * N + Q::Y, yl);
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-        S acc = v[i];
-#pragma unroll
-        for (int m = 0; m < B; ++m) acc = fnma_(Y1[i][m], yl[m], acc);
-        t[i] = acc;
-      }
-      if (o + h < K) {
-        S Y2[B][B], yr[B];
-        rld_full<B, S>(po + Q::Y2, Y2);
-        rld_v<B, S>(sep + (o + h) * N + Q::Y, yr);
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-          S acc = t[i];
-#pragma unroll
-          for (int m = 0; m < B; ++m) acc = fnma_(Y2[i][m], yr[m], acc);
-          t[i] = acc;
-        }
-      }
-      lltsolve<B, S>(Lf, t, y);
-      rst_v<B, S>(sep + o * N + Q::Y, y);
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------ PCR ---
-// Parallel cyclic reduction of the K x K block-tridiagonal SPD separator
-// system, one separator per thread, its blocks kept in registers:
-//   D_i (diagonal), Bl_i = block (i, i-h), Cr_i = block (i, i+h), r_i.
-// Level h: every thread factors D_i = L_i L_i^T and publishes
-//   F_i = L_i^{-1} Bl_i,  E_i = L_i^{-1} Cr_i,  g_i = L_i^{-1} r_i;
-// then eliminates its neighbours i -+ h from its own equation:
-//   D_i -= E_{i-h}^T E_{i-h} + F_{i+h}^T F_{i+h},  r_i -= E_{i-h}^T g_{i-h} + F_{i+h}^T g_{i+h},
-//   Bl_i = -E_{i-h}^T F_{i-h} (couples i-2h),  Cr_i = -F_{i+h}^T E_{i+h} (couples i+2h).
-// Each equation becomes a Schur complement of the SPD system, so every D_i
-// stays SPD; after ceil(log2 K) levels the system is block diagonal and
-// y_i = D_i^{-1} r_i.  The published triples alternate between two buffers,
-// so a level costs one barrier.  Record of separator i (PRec<B>::N values):
-// [buffer 0: F E g][buffer 1: F E g][y]; buffer 0 first carries the pass-1
-// hand-over (A_ll lower, A_rl, r_l) of the chunk to the right of the separator.
-template <int B>
-struct PRec {
-  static constexpr int W = 2 * B * B + B;
-  static constexpr int N = (2 * W + B) | 1;
-  static constexpr int F = 0, E = B * B, G = 2 * B * B, Y = 2 * W;
-  static constexpr int HA = F, HB = E, HR = G;  // pass-1 hand-over (buffer 0)
-  static constexpr bool shared_handover = false;
-};
-
-template <int B, class S>
-__device__ __forceinline__ void rpcr(S* rec, int K, int k, const int* stime, int* sfail, S (&D)[B][B],
-                                     S (&Bl)[B][B], S (&Cr)[B][B], S (&r)[B], S (&y)[B]) {
-  using Q = PRec<B>;
-  int bad = 0;
-  int lev = 0;
-#pragma unroll 1
-  for (int h = 1; h < K; h <<= 1, ++lev) {
-    const int bo = (lev & 1) ? 0 : Q::W;  // level 0 writes buffer 1 (buffer 0 holds the hand-over)
-    {
-      S Lf[B][B], F[B][B], E[B][B], gv[B];
-      bad |= lchol<B, S>(D, Lf);
-      lleft<B, S>(Lf, Bl, F);
-      lleft<B, S>(Lf, Cr, E);
-      llsolve<B, S>(Lf, r, gv);
-      S* pk = rec + k * Q::N + bo;
-      rst_full<B, S>(pk + Q::F, F);
-      rst_full<B, S>(pk + Q::E, E);
-      rst_v<B, S>(pk + Q::G, gv);
-    }
-    __syncthreads();
-    if (k - h >= 0) {
-      const S* pl = rec + (k - h) * Q::N + bo;
-      S El[B][B], Fl[B][B], gl[B];
-      rld_full<B, S>(pl + Q::E, El);
-      rld_full<B, S>(pl + Q::F, Fl);
-      rld_v<B, S>(pl + Q::G, gl);
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-#pragma unroll
-        for (int j = 0; j <= i; ++j) {
-          S a = D[i][j];
-#pragma unroll
-          for (int m = 0; m < B; ++m) a = fnma_(El[m][i], El[m][j], a);
-          D[i][j] = a;
-        }
-        S ar = r[i];
-#pragma unroll
-        for (int m = 0; m < B; ++m) ar = fnma_(El[m][i], gl[m], ar);
-        r[i] = ar;
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          S a = mul_(El[0][i], Fl[0][j]);
-#pragma unroll
-          for (int m = 1; m < B; ++m) a = fma_(El[m][i], Fl[m][j], a);
-          Bl[i][j] = neg_(a);
-        }
-      }
-    } else {
-      zero<B, S>(Bl);
-    }
-    if (k + h < K) {
-      const S* pr = rec + (k + h) * Q::N + bo;
-      S Fr[B][B], Er[B][B], gr[B];
-      rld_full<B, S>(pr + Q::F, Fr);
-      rld_full<B, S>(pr + Q::E, Er);
-      rld_v<B, S>(pr + Q::G, gr);
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-#pragma unroll
-        for (int j = 0; j <= i; ++j) {
-          S a = D[i][j];
-#pragma unroll
-          for (int m = 0; m < B; ++m) a = fnma_(Fr[m][i], Fr[m][j], a);
-          D[i][j] = a;
-        }
-        S ar = r[i];
-#pragma unroll
-        for (int m = 0; m < B; ++m) ar = fnma_(Fr[m][i], gr[m], ar);
-        r[i] = ar;
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          S a = mul_(Fr[0][i], Er[0][j]);
-#pragma unroll
-          for (int m = 1; m < B; ++m) a = fma_(Fr[m][i], Er[m][j], a);
-          Cr[i][j] = neg_(a);
-        }
-      }
-    } else {
-      zero<B, S>(Cr);
-    }
-  }
-  S Lf[B][B], t[B];
-  bad |= lchol<B, S>(D, Lf);
-  llsolve<B, S>(Lf, r, t);
-  lltsolve<B, S>(Lf, t, y);
-  if (bad) report<1>(sfail, bad, stime[k]);
-  rst_v<B, S>(rec + k * Q::N + Q::Y, y);
-  __syncthreads();
-}
-
 // ------------------------------------------------- BCR, registers resident ---
 // Block cyclic reduction with every separator's blocks in its thread's
 // registers (D, Bl = block (i, i-h), Cr = block (i, i+h), r).  At level h the
@@ -579,368 +279,16 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
 }
 
 
-// ------------------------------------------------ warp-level separator solve ---
-template <class S>
-__device__ __forceinline__ S shfl_(S v, int src) { return __shfl_sync(0xffffffffu, v, src); }
-template <int B, class S>
-__device__ __forceinline__ void shfl_m(const S (&a)[B][B], int src, S (&o)[B][B]) {
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int j = 0; j < B; ++j) o[i][j] = shfl_(a[i][j], src);
-}
-template <int B, class S>
-__device__ __forceinline__ void shfl_v(const S (&a)[B], int src, S (&o)[B]) {
-#pragma unroll
-  for (int i = 0; i < B; ++i) o[i] = shfl_(a[i], src);
-}
-
-// The K x K separator system of one instance solved by ONE warp (all 32 lanes
-// call it): lane l owns separators l m .. l m + m - 1 (m = K / 32 <= MS),
-// eliminates the first m - 1 (block Cholesky with the spike towards
-// super-separator l - 1, as pipe_sep2_kernel), the 32 super-separators are
-// reduced by block cyclic reduction with warp shuffles -- no shared memory
-// round trip, no CTA barrier per level -- and the owned separators are
-// recovered by forward + back substitution.  in: field-major separator blocks
-// [PSep<B>::N][K] with A_ll / r_l for every separator (psep_ld NT = 1);
-// yo: [B][K] output; scratch: 32 * (B(B+1)/2 + 2 B^2 + B) values for the
-// super-separators' factors (kept for the back substitution).
-template <int B, class S, int MS>
-__device__ __forceinline__ void rsep_warp(const S* in, int K, int T, S* yo, S* scratch, int lane, int* sfail) {
-  const int m = K / 32;
-  const int j0 = lane * m, js = j0 + m - 1;
-  int cf = INT_MAX;
-  S Lr[MS - 1][B][B];
-  S Lc[B][B], wv[B], X[B][B], All[B][B], rl[B];
-  zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
-  S sg = splat<S>(1.0);
-#pragma unroll
-  for (int i = 0; i < MS - 1; ++i) {
-    if (i < m - 1) {
-      S D[B][B], r[B], Bl[B][B];
-      psep_ld<B, S>(in, K, 1, j0 + i, D, r, Bl);
-      if (i == 0) {
-        lchol<B, S>(D, Lc);
-        llsolve<B, S>(Lc, r, wv);
-        lleft<B, S>(Lc, Bl, X);
-#pragma unroll
-        for (int a = 0; a < B; ++a) {
-#pragma unroll
-          for (int q = 0; q <= a; ++q) {
-            S acc = mul_(X[0][a], X[0][q]);
-#pragma unroll
-            for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
-            All[a][q] = acc;
-          }
-          S acc = mul_(X[0][a], wv[0]);
-#pragma unroll
-          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
-          rl[a] = acc;
-        }
-      } else {
-        S Pm[B][B];
-#pragma unroll
-        for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pm[a]);
-        lcouple<B, S>(Pm, wv, D, r);
-        lchol<B, S>(D, Lc);
-        llsolve<B, S>(Lc, r, wv);
-        S Y[B][B];
-#pragma unroll
-        for (int a = 0; a < B; ++a)
-#pragma unroll
-          for (int q = 0; q < B; ++q) {
-            S acc = mul_(Pm[a][0], X[0][q]);
-#pragma unroll
-            for (int mm = 1; mm < B; ++mm) acc = fma_(Pm[a][mm], X[mm][q], acc);
-            Y[a][q] = acc;
-          }
-        lleft<B, S>(Lc, Y, X);
-        sg = neg_(sg);
-#pragma unroll
-        for (int a = 0; a < B; ++a) {
-#pragma unroll
-          for (int q = 0; q <= a; ++q) {
-            S acc = All[a][q];
-#pragma unroll
-            for (int mm = 0; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
-            All[a][q] = acc;
-          }
-          S acc = mul_(X[0][a], wv[0]);
-#pragma unroll
-          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
-          rl[a] = fma_(sg, acc, rl[a]);
-        }
-      }
-      rcopyL<B, S>(Lc, Lr[i]);
-    }
-  }
-  S Ds[B][B], Rs[B], Bs[B][B], Cs[B][B];
-  {
-    S Bl[B][B];
-    psep_ld<B, S>(in, K, 1, js, Ds, Rs, Bl);
-    if (m > 1) {
-      S Pl[B][B];
-#pragma unroll
-      for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pl[a]);
-      lcouple<B, S>(Pl, wv, Ds, Rs);
-#pragma unroll
-      for (int a = 0; a < B; ++a)
-#pragma unroll
-        for (int q = 0; q < B; ++q) {
-          S acc = mul_(Pl[a][0], X[0][q]);
-#pragma unroll
-          for (int mm = 1; mm < B; ++mm) acc = fma_(Pl[a][mm], X[mm][q], acc);
-          Bs[a][q] = mul_(neg_(sg), acc);
-        }
-      if (bad_(splat<S>(1.0) / Lc[B - 1][B - 1])) cf = 1 + (chunk_begin(j0 + 1, T, K) - 1);
-    } else {
-#pragma unroll
-      for (int a = 0; a < B; ++a)
-#pragma unroll
-        for (int q = 0; q < B; ++q) Bs[a][q] = Bl[a][q];
-    }
-  }
-  {  // hand-over from lane l + 1: A_ll, r_l onto this super-separator, coupling C = B_{l+1}^T
-    S Al[B][B], Bn[B][B], rr[B];
-#pragma unroll
-    for (int a = 0; a < B; ++a) {
-      rl[a] = neg_(rl[a]);
-#pragma unroll
-      for (int q = 0; q <= a; ++q) {
-        All[a][q] = neg_(All[a][q]);
-        All[q][a] = All[a][q];
-      }
-    }
-    const int src = lane + 1 < 32 ? lane + 1 : lane;
-    shfl_m<B, S>(All, src, Al);
-    shfl_m<B, S>(Bs, src, Bn);
-    shfl_v<B, S>(rl, src, rr);
-    if (lane + 1 < 32) {
-#pragma unroll
-      for (int a = 0; a < B; ++a) {
-        Rs[a] = add_(Rs[a], rr[a]);
-#pragma unroll
-        for (int q = 0; q <= a; ++q) Ds[a][q] = add_(Ds[a][q], Al[a][q]);
-#pragma unroll
-        for (int q = 0; q < B; ++q) Cs[a][q] = Bn[q][a];
-      }
-    } else {
-      zero<B, S>(Cs);
-    }
-  }
-  // ---- block cyclic reduction over the 32 lanes
-  constexpr int LT = B * (B + 1) / 2, SN = LT + 2 * B * B + B;
-  S* my = scratch + lane * SN;  // factors of this lane's elimination level: L, F, E, g
-  int myh = 0;
-  int bad = 0;
-#pragma unroll 1
-  for (int h = 1; h < 32; h <<= 1) {
-    const int lv = lane & (2 * h - 1);
-    S F[B][B], E[B][B], gv[B];
-    zero<B, S>(F); zero<B, S>(E); zero<B, S>(gv);
-    if (lv == h) {
-      S Lf[B][B];
-      bad |= lchol<B, S>(Ds, Lf);
-      lleft<B, S>(Lf, Bs, F);
-      lleft<B, S>(Lf, Cs, E);
-      llsolve<B, S>(Lf, Rs, gv);
-      rst_tri<B, S>(my, Lf);
-      rst_full<B, S>(my + LT, F);
-      rst_full<B, S>(my + LT + B * B, E);
-      rst_v<B, S>(my + LT + 2 * B * B, gv);
-      myh = h;
-    }
-    const int sl = lane - h >= 0 ? lane - h : lane, sr = lane + h < 32 ? lane + h : lane;
-    S El[B][B], Fl[B][B], gl[B], Fr[B][B], Er[B][B], gr[B];
-    shfl_m<B, S>(E, sl, El);
-    shfl_m<B, S>(F, sl, Fl);
-    shfl_v<B, S>(gv, sl, gl);
-    shfl_m<B, S>(F, sr, Fr);
-    shfl_m<B, S>(E, sr, Er);
-    shfl_v<B, S>(gv, sr, gr);
-    if (lv == 0) {
-      if (lane - h >= 0) {
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-#pragma unroll
-          for (int j = 0; j <= i; ++j) {
-            S a = Ds[i][j];
-#pragma unroll
-            for (int q = 0; q < B; ++q) a = fnma_(El[q][i], El[q][j], a);
-            Ds[i][j] = a;
-          }
-          S ar = Rs[i];
-#pragma unroll
-          for (int q = 0; q < B; ++q) ar = fnma_(El[q][i], gl[q], ar);
-          Rs[i] = ar;
-#pragma unroll
-          for (int j = 0; j < B; ++j) {
-            S a = mul_(El[0][i], Fl[0][j]);
-#pragma unroll
-            for (int q = 1; q < B; ++q) a = fma_(El[q][i], Fl[q][j], a);
-            Bs[i][j] = neg_(a);
-          }
-        }
-      }
-      if (lane + h < 32) {
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-#pragma unroll
-          for (int j = 0; j <= i; ++j) {
-            S a = Ds[i][j];
-#pragma unroll
-            for (int q = 0; q < B; ++q) a = fnma_(Fr[q][i], Fr[q][j], a);
-            Ds[i][j] = a;
-          }
-          S ar = Rs[i];
-#pragma unroll
-          for (int q = 0; q < B; ++q) ar = fnma_(Fr[q][i], gr[q], ar);
-          Rs[i] = ar;
-#pragma unroll
-          for (int j = 0; j < B; ++j) {
-            S a = mul_(Fr[0][i], Er[0][j]);
-#pragma unroll
-            for (int q = 1; q < B; ++q) a = fma_(Fr[q][i], Er[q][j], a);
-            Cs[i][j] = neg_(a);
-          }
-        }
-      } else {
-        zero<B, S>(Cs);
-      }
-    }
-  }
-  S y[B];
-  zero<B, S>(y);
-  if (lane == 0) {
-    S Lf[B][B], t[B];
-    bad |= lchol<B, S>(Ds, Lf);
-    llsolve<B, S>(Lf, Rs, t);
-    lltsolve<B, S>(Lf, t, y);
-  }
-  if (bad) cf = min(cf, 1 + (chunk_begin(js + 1, T, K) - 1));
-#pragma unroll 1
-  for (int h = 16; h >= 1; h >>= 1) {
-    const int sl = lane - h >= 0 ? lane - h : lane, sr = lane + h < 32 ? lane + h : lane;
-    S yl[B], yr[B];
-    shfl_v<B, S>(y, sl, yl);
-    shfl_v<B, S>(y, sr, yr);
-    if (myh == h) {
-      S Lf[B][B], F[B][B], t[B];
-      rld_tri<B, S>(my, Lf);
-      rld_full<B, S>(my + LT, F);
-      rld_v<B, S>(my + LT + 2 * B * B, t);
-#pragma unroll
-      for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int q = 0; q < B; ++q) t[i] = fnma_(F[i][q], yl[q], t[i]);
-      if (lane + h < 32) {
-        S E[B][B];
-        rld_full<B, S>(my + LT + B * B, E);
-#pragma unroll
-        for (int i = 0; i < B; ++i)
-#pragma unroll
-          for (int q = 0; q < B; ++q) t[i] = fnma_(E[i][q], yr[q], t[i]);
-      }
-      lltsolve<B, S>(Lf, t, y);
-    }
-  }
-  if (cf != INT_MAX) atomicMin(sfail, cf);
-  // ---- recover the owned separators
-  S yL[B];
-  shfl_v<B, S>(y, lane > 0 ? lane - 1 : 0, yL);
-  if (lane == 0) zero<B, S>(yL);
-#pragma unroll
-  for (int a = 0; a < B; ++a) yo[a * K + js] = y[a];
-  S Wp[MS - 1][B];
-#pragma unroll
-  for (int i = 0; i < MS - 1; ++i) {
-    if (i < m - 1) {
-      S r[B], Bl[B][B], tv[B], u[B];
-      psep_ld_rb<B, S>(in, K, 1, j0 + i, r, Bl);
-      if (i == 0) {
-#pragma unroll
-        for (int a = 0; a < B; ++a) tv[a] = yL[a];
-      } else {
-        lltsolve<B, S>(Lr[i - 1], Wp[i - 1], tv);
-      }
-#pragma unroll
-      for (int a = 0; a < B; ++a) {
-        S acc = r[a];
-#pragma unroll
-        for (int q = 0; q < B; ++q) acc = fnma_(Bl[a][q], tv[q], acc);
-        u[a] = acc;
-      }
-      llsolve<B, S>(Lr[i], u, Wp[i]);
-    }
-  }
-  S yn[B];
-#pragma unroll
-  for (int a = 0; a < B; ++a) yn[a] = y[a];
-#pragma unroll
-  for (int i = MS - 2; i >= 0; --i) {
-    if (i < m - 1) {
-      S Bn[B][B], v[B], u[B], tv[B], yv[B];
-      psep_ld_b<B, S>(in, K, j0 + i + 1, Bn);
-#pragma unroll
-      for (int a = 0; a < B; ++a) {
-        S acc = mul_(Bn[0][a], yn[0]);
-#pragma unroll
-        for (int q = 1; q < B; ++q) acc = fma_(Bn[q][a], yn[q], acc);
-        v[a] = acc;
-      }
-      llsolve<B, S>(Lr[i], v, u);
-#pragma unroll
-      for (int a = 0; a < B; ++a) tv[a] = sub_(Wp[i][a], u[a]);
-      lltsolve<B, S>(Lr[i], tv, yv);
-#pragma unroll
-      for (int a = 0; a < B; ++a) yo[a * K + j0 + i] = yv[a];
-#pragma unroll
-      for (int a = 0; a < B; ++a) yn[a] = yv[a];
-    }
-  }
-}
-
-template <int B, int SEP> struct RfSep { using R = BRec<B>; };
-template <int B> struct RfSep<B, 1> { using R = PRec<B>; };
-template <int B> struct RfSep<B, 0> { using R = RRec<B>; };
-
-
-// Thread -> chunk map: chunks ordered by the level at which the separator
-// reduction eliminates them (odd k first, then k = 2 mod 4, 4 mod 8, ...,
-// k = 0 last), so that at every level the eliminating and the surviving
-// separators sit in different warps and the reduction's two code paths do
-// not both run in every warp (levels >= 3 touch only the last warp for K=128).
-__device__ __forceinline__ int rf_chunk_of_thread(int t, int K) {
-  int h = 1, start = 0;
-  while (h < K) {
-    const int n = (K - h + 2 * h - 1) / (2 * h);  // #{k = h (mod 2h), k < K}
-    if (t < start + n) return h + 2 * h * (t - start);
-    start += n;
-    h <<= 1;
-  }
-  return 0;
-}
-
-// SEG = false: the interior factors stay in registers from pass 1 to pass 2
-// (chunks of <= CM = RfCM points).  SEG = true: pass 1 keeps nothing
-// (p1_chunk) and pass 2 re-factors in register segments (p2_chunk), so chunks
-// can be twice as long (CM = 2 PipeHM + 1): half the separators, half the
-// threads per instance, twice the instances per SM.
-template <int B, class Tio, class S, bool BWD, int CM, bool SEG = false>
-__global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMNN_RF_MIN_BLOCKS)
-    rf_kernel(Args<Tio> a, RLayout L) {
+// The interior factors stay in registers from pass 1 to pass 2 (chunks of
+// <= CM points; CM = RfCM, or RfCMW for the wide variant).
+template <int B, class Tio, class S, bool BWD, int CM>
+__global__ void __launch_bounds__(SMNN_RF_MAX_THREADS, SMNN_RF_MIN_BLOCKS) rf_kernel(Args<Tio> a, RLayout L) {
   unsigned char* sm = smnn_dyn_smem;
   Tio* smT = reinterpret_cast<Tio*>(sm);
   const int nt = blockDim.x, K = nt;
-  // RF_MAP 2: odd chunks (the separators the first reduction level eliminates)
-  // in the first half of the CTA, even ones in the second half, so that level
-  // 1 runs one code path per warp and levels >= 2 run on half of the warps
-  const int k = RF_MAP == 1 ? rf_chunk_of_thread(int(threadIdx.x), K)
-              : RF_MAP == 2 ? (int(threadIdx.x) < K / 2 ? 2 * int(threadIdx.x) + 1 : 2 * (int(threadIdx.x) - K / 2))
-                            : int(threadIdx.x);
+  const int k = int(threadIdx.x);
   const int T = a.T;
-  using Q = RRec<B>;
-  using R2 = typename RfSep<B, SMNN_RF_SEP>::R;
+  using R2 = BRec<B>;
   S* sep = reinterpret_cast<S*>(sm + L.off_sep);  // K separator records
   int* stime = reinterpret_cast<int*>(sm + L.off_ck);  // after the record region
   int* sfail = stime + nt;
@@ -951,8 +299,6 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
   uint32_t parity = 0;
   const int f = chunk_begin(k, T, K), sig = chunk_begin(k + 1, T, K) - 1;
   const int nint = sig - f;  // interior points, 1 <= nint <= CM - 1 (host guarantees)
-  // separator system solved by one warp (rsep_warp) when it has <= 4 separators per lane
-  const bool wsolve = RF_WARP_SEP && SMNN_RF_SEP == 2 && K % 32 == 0 && K <= 128;
   constexpr int E = int(sizeof(Tio));
 
   for (int64_t g = blockIdx.x; g < a.n_inst; g += gridDim.x) {
@@ -1011,18 +357,10 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
     // ================================================================ pass 1
     S Lr[CM - 1][B][B];
     S Dsep[B][B], Rsep[B];
-#if SMNN_RF_SEP != 0
     S Bsep[B][B], Csep[B][B];
-#endif
     {
       S All[B][B], rl[B], Arl[B][B];
       int bad = 0, badj = INT_MAX;
-      if constexpr (SEG) {
-        if (p1_chunk<B, Tio, S, BWD, CM>(w, x.n_iv, x.u[0], k, K, nint, cS, dS, sS, gS, Dsep, Rsep, Arl, All, rl)) {
-          bad = 1;
-          badj = f;
-        }
-      } else {
       S ap[2 * B - 1];
       if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
       S Lc[B][B], wv[B], X[B][B];
@@ -1146,7 +484,6 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
         }
         lcouple<B, S>(Pl, wv, Dsep, Rsep);
       }
-      }  // !SEG
       // A_ll = -sum X^T X and r_l = -sum X^T w belong to sigma_{k-1}: hand them over.
 #pragma unroll
       for (int r = 0; r < B; ++r) {
@@ -1157,58 +494,6 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
           All[q][r] = All[r][q];
         }
       }
-#if SMNN_RF_SEP == 0
-      S* pk = sep + k * Q::N;
-      rst_low<B, S>(pk + Q::Y2, All);
-      rst_v<B, S>(pk + Q::Y, rl);
-      rst_full<B, S>(pk + Q::BC, Arl);
-      if (bad) report<1>(sfail, bad, badj);
-    }
-    __syncthreads();
-    if (k + 1 < K) {  // add the right neighbour's A_ll, r_l
-      S Al[B][B], rr[B];
-      const S* pn = sep + (k + 1) * Q::N;
-      rld_low<B, S>(pn + Q::Y2, Al);
-      rld_v<B, S>(pn + Q::Y, rr);
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        Rsep[r] = add_(Rsep[r], rr[r]);
-#pragma unroll
-        for (int q = 0; q <= r; ++q) Dsep[r][q] = add_(Dsep[r][q], Al[r][q]);
-      }
-    }
-    // D / R are other fields of the record than the Y2 / Y the left neighbour reads
-    rst_low<B, S>(sep + k * Q::N + Q::D, Dsep);
-    rst_v<B, S>(sep + k * Q::N + Q::R, Rsep);
-    __syncthreads();
-    rbcr<B, S>(sep, stime, sfail, K, k);
-    S yL[B], yR[B];
-    rld_v<B, S>(sep + k * Q::N + Q::Y, yR);
-    if (k > 0) rld_v<B, S>(sep + (k - 1) * Q::N + Q::Y, yL); else zero<B, S>(yL);
-#else
-      if (wsolve) {  // field-major separator blocks for the one-warp solve (rsep_warp)
-        using PS = PSep<B>;
-        S* o = sep + k;
-        int e = 0;
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-#pragma unroll
-          for (int q = 0; q <= r; ++q) o[(PS::D + e++) * K] = Dsep[r][q];
-#pragma unroll
-        for (int r = 0; r < B; ++r) o[(PS::R + r) * K] = Rsep[r];
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-#pragma unroll
-          for (int q = 0; q < B; ++q) o[(PS::BL + r * B + q) * K] = Arl[r][q];
-        e = 0;
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-#pragma unroll
-          for (int q = 0; q <= r; ++q) o[(PS::AL + e++) * K] = All[r][q];
-#pragma unroll
-        for (int r = 0; r < B; ++r) o[(PS::RL + r) * K] = rl[r];
-        if (bad) report<1>(sfail, bad, badj);
-      } else {
       S* pk = sep + k * R2::N;  // hand-over to separator k-1
       rst_tri<B, S>(pk + R2::HA, All);
       rst_full<B, S>(pk + R2::HB, Arl);
@@ -1218,22 +503,10 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
       for (int r = 0; r < B; ++r)
 #pragma unroll
         for (int q = 0; q < B; ++q) Bsep[r][q] = Arl[r][q];
-      }  // !wsolve
     }
     __syncthreads();
     RF_STAMP(2);
     S yL[B], yR[B];
-    if (wsolve) {
-      S* yo = sep + PSep<B>::N * K;
-      if (threadIdx.x < 32)
-        rsep_warp<B, S, 4>(sep, K, T, yo, yo + B * K, int(threadIdx.x), sfail);
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        yR[r] = yo[r * K + k];
-        yL[r] = k > 0 ? yo[r * K + k - 1] : splat<S>(0.0);
-      }
-    } else {
     if (k + 1 < K) {  // the right chunk's A_ll, r_l and the coupling to sigma_{k+1}
       S Al[B][B], An[B][B], rr[B];
       const S* pn = sep + (k + 1) * R2::N;
@@ -1251,17 +524,10 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
     } else {
       zero<B, S>(Csep);
     }
-#if SMNN_RF_SEP == 1
-    __syncthreads();  // hand-over slots are PCR buffer 0
-    rpcr<B, S>(sep, K, k, stime, sfail, Dsep, Bsep, Csep, Rsep, yR);
-#else
     if (R2::shared_handover) __syncthreads();  // hand-over read before level 1 publishes
     rbcr2<B, S>(sep, K, k, stime, sfail, Dsep, Bsep, Csep, Rsep);
     rld_v<B, S>(sep + k * R2::N + R2::Y, yR);
-#endif
     if (k > 0) rld_v<B, S>(sep + (k - 1) * R2::N + R2::Y, yL); else zero<B, S>(yL);
-    }  // !wsolve
-#endif
 
     if (LATE_Y) {  // every thread has read its separator values: the records may go
       __syncthreads();
@@ -1273,13 +539,6 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
     }
     RF_STAMP(3);
     // ================================================================ pass 2
-    if constexpr (SEG) {
-      if (LATE_Y) {
-        mbar_wait(bar, parity);
-        parity ^= 1u;
-      }
-      p2_chunk<B, Tio, S, BWD, CM>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR);
-    } else {
     // forward substitution with both separator values known
     // w'_i goes to shared memory, in place over the step's consumed right-hand
     // side input (c_i forward -- y_i overwrites it afterwards; dl/dy_i backward)
@@ -1390,7 +649,6 @@ __global__ void __launch_bounds__(SEG ? 256 : SMNN_RF_MAX_THREADS, SEG ? 2 : SMN
         stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL, yfm, yn, yfn));
       }
     }
-    }  // !SEG
     RF_STAMP(4);
     // ---- write the outputs back: TMA bulk store of the 16-byte aligned body,
     //      plain stores for the unaligned head / tail elements

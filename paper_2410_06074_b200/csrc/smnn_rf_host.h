@@ -5,11 +5,35 @@
 
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 #include "smnn.h"
 
 namespace smnn {
+
+// Raise a kernel's dynamic shared-memory limit to at least `smem` on the
+// CURRENT device (the attribute is per device; the cache is keyed by
+// (device, kernel) and keeps the largest request made so far).
+inline cudaError_t ensure_smem(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> top;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& t = top[std::make_pair(dev, kern)];
+  if (smem <= t) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e == cudaSuccess) t = smem;
+  return e;
+}
+template <class Kern>
+cudaError_t ensure_smem_k(Kern* k, size_t smem) {
+  return ensure_smem(reinterpret_cast<const void*>(k), smem);
+}
 
 // Arguments of the fused kernels (device pointers; see include/smnn.h).
 template <class Tio>

@@ -44,14 +44,24 @@ def _dtype_code(t: torch.Tensor, compute: str | None) -> int:
     raise TypeError(f"unsupported dtype {t.dtype}: use float32 or float64")
 
 
-def _problem(coeffs, iv, w: Weights, compute, threads_per_inst=0) -> _abi.smnn_problem:
+def _path_code(path) -> int:
+    if path is None:
+        return 0
+    if isinstance(path, str):
+        if path not in _abi.PATH_CODES:
+            raise ValueError(f"unknown kernel path {path!r}: one of {sorted(_abi.PATH_CODES)}")
+        return _abi.PATH_CODES[path]
+    return int(path)
+
+
+def _problem(coeffs, iv, w: Weights, compute, threads_per_inst=0, path=None) -> _abi.smnn_problem:
     if coeffs.dim() < 2:
         raise ValueError("coeffs must be [..., T, R+1]")
     T, R1 = coeffs.shape[-2], coeffs.shape[-1]
     n_inst = coeffs.numel() // max(T * R1, 1)
     return _abi.smnn_problem(
         n_inst=n_inst, T=T, order=R1 - 1, n_iv=iv.shape[-1], dtype=_dtype_code(coeffs, compute),
-        threads_per_inst=threads_per_inst, reserved=0,
+        threads_per_inst=threads_per_inst, path=_path_code(path),
         w_gov=float(w.gov), w_init=float(w.init), w_smooth=float(w.smooth))
 
 
@@ -84,11 +94,11 @@ def _stream(device) -> int:
 
 
 def kernel_path(n_inst: int, T: int, order: int, n_iv: int, dtype=torch.float32, compute=None, bwd=False,
-                w: Weights = Weights()) -> str:
-    """Kernel path ("rf" | "pipe" | "checkpoint") smnn_kernel_path reports for a problem shape."""
+                w: Weights = Weights(), path=None) -> str:
+    """Kernel path ("rf" | "pipe" | "checkpoint" | "x64") smnn_kernel_path reports for a problem shape."""
     code = _abi.SMNN_F64 if dtype == torch.float64 else (_abi.SMNN_F32_C64 if compute == "f64" else _abi.SMNN_F32)
-    p = _abi.smnn_problem(n_inst=n_inst, T=T, order=order, n_iv=n_iv, dtype=code, threads_per_inst=0, reserved=0,
-                          w_gov=w.gov, w_init=w.init, w_smooth=w.smooth)
+    p = _abi.smnn_problem(n_inst=n_inst, T=T, order=order, n_iv=n_iv, dtype=code, threads_per_inst=0,
+                          path=_path_code(path), w_gov=w.gov, w_init=w.init, w_smooth=w.smooth)
     r = _abi.load().smnn_kernel_path(ctypes.byref(p), int(bool(bwd)))
     _abi.check(min(r, 0), "smnn_kernel_path")
     return _abi.PATH_NAMES[r]
@@ -119,11 +129,13 @@ def smnn_assemble(coeffs, rhs, iv, steps, w: Weights = Weights(), compute=None):
     return M, N, beta
 
 
-def smnn_factor_solve_fwd(coeffs, rhs, iv, steps, w: Weights = Weights(), compute=None, threads_per_inst=0):
-    """Fused Algorithm 1: returns (y [..., T, b], info [n_inst] int32)."""
+def smnn_factor_solve_fwd(coeffs, rhs, iv, steps, w: Weights = Weights(), compute=None, threads_per_inst=0,
+                          path=None):
+    """Fused Algorithm 1: returns (y [..., T, b], info [n_inst] int32).  `path` forces a kernel path
+    ("rf" | "pipe" | "x64" | "resident" | "stream"; default automatic)."""
     _check_inputs(coeffs, rhs, iv, steps)
     coeffs, rhs, iv, steps = map(_c, (coeffs, rhs, iv, steps))
-    p = _problem(coeffs, iv, w, compute, threads_per_inst)
+    p = _problem(coeffs, iv, w, compute, threads_per_inst, path)
     with torch.cuda.device(coeffs.device):
         y = torch.empty_like(coeffs)
         info = torch.empty(p.n_inst, dtype=torch.int32, device=coeffs.device)
@@ -135,13 +147,18 @@ def smnn_factor_solve_fwd(coeffs, rhs, iv, steps, w: Weights = Weights(), comput
 
 
 def smnn_solve_bwd(coeffs, rhs, iv, steps, y, grad_y, w: Weights = Weights(), compute=None, threads_per_inst=0,
-                   need=(True, True, True, True)):
+                   need=(True, True, True, True), path=None):
     """Fused Algorithm 2 + chain rule: returns (dcoeffs, drhs, div, dsteps, info)."""
     _check_inputs(coeffs, rhs, iv, steps)
     coeffs, rhs, iv, steps, y, grad_y = map(_c, (coeffs, rhs, iv, steps, y, grad_y))
-    if y.shape != coeffs.shape or grad_y.shape != coeffs.shape:
-        raise ValueError("y and grad_y must have the shape of coeffs")
-    p = _problem(coeffs, iv, w, compute, threads_per_inst)
+    for name, t in (("y", y), ("grad_y", grad_y)):
+        if t.shape != coeffs.shape:
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(coeffs.shape)}")
+        if t.dtype != coeffs.dtype:
+            raise TypeError(f"{name} dtype {t.dtype} != coeffs dtype {coeffs.dtype}")
+        if t.device != coeffs.device:
+            raise ValueError(f"{name} is on {t.device}, coeffs on {coeffs.device}")
+    p = _problem(coeffs, iv, w, compute, threads_per_inst, path)
     with torch.cuda.device(coeffs.device):
         dc = torch.empty_like(coeffs) if need[0] else None
         dd = torch.empty_like(rhs) if need[1] else None
@@ -179,8 +196,14 @@ def smnn_factor(coeffs, iv, steps, w: Weights = Weights(), compute=None):
 def smnn_substitute(L, P, alpha, n_iv=1, compute=None):
     """Algorithm 4 with materialised L, P: returns M^{-1} alpha."""
     L, P, alpha = map(_c, (L, P, alpha))
-    if not (L.is_cuda and alpha.is_cuda):
+    if not (L.is_cuda and P.is_cuda and alpha.is_cuda):
         raise RuntimeError("L, P, alpha must be CUDA tensors")
+    lead, T, b = alpha.shape[:-2], alpha.shape[-2], alpha.shape[-1]
+    for name, t, shape in (("L", L, (*lead, T, b, b)), ("P", P, (*lead, max(T - 1, 0), b, b))):
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+        if t.dtype != alpha.dtype or t.device != alpha.device:
+            raise TypeError(f"{name} must match alpha's dtype and device")
     p = _problem(alpha, alpha[..., :1, :n_iv], Weights(), compute)
     with torch.cuda.device(alpha.device):
         out = torch.empty_like(alpha)
@@ -222,15 +245,33 @@ class HostPlan:
         self.device = torch.device(device or "cuda")
         code = _abi.SMNN_F64 if dtype == torch.float64 else (_abi.SMNN_F32_C64 if compute == "f64" else _abi.SMNN_F32)
         self.p = _abi.smnn_problem(n_inst=n_inst, T=T, order=order, n_iv=n_iv, dtype=code, threads_per_inst=0,
-                                   reserved=0, w_gov=w.gov, w_init=w.init, w_smooth=w.smooth)
+                                   path=0, w_gov=w.gov, w_init=w.init, w_smooth=w.smooth)
         self.h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _abi.check(_abi.load().smnn_plan_create(ctypes.byref(self.h), ctypes.byref(self.p)), "smnn_plan_create")
 
+    def _expect(self):
+        n, T, b, niv = self.p.n_inst, self.p.T, self.p.order + 1, self.p.n_iv
+        return {"coeffs": n * T * b, "rhs": n * T, "iv": n * niv, "steps": n * max(T - 1, 0), "grad_y": n * T * b,
+                "y": n * T * b, "dc": n * T * b, "dd": n * T, "du": n * niv, "ds": n * max(T - 1, 0)}
+
     def fwd_bwd(self, coeffs, rhs, iv, steps, grad_y, y, dc, dd, du, ds, info=None, stream=None):
-        for t in (coeffs, rhs, iv, steps, grad_y, y, dc, dd, du, ds):
-            if t.is_cuda:
-                raise ValueError("HostPlan takes host (CPU, ideally pinned) tensors")
+        """Every tensor must be a contiguous CPU tensor (ideally pinned) of the plan's dtype and
+        element count: the library copies exactly that many bytes to / from the raw pointers."""
+        want = torch.float64 if self.p.dtype == _abi.SMNN_F64 else torch.float32
+        size = self._expect()
+        for name, t in (("coeffs", coeffs), ("rhs", rhs), ("iv", iv), ("steps", steps), ("grad_y", grad_y),
+                        ("y", y), ("dc", dc), ("dd", dd), ("du", du), ("ds", ds)):
+            if t is None:
+                raise ValueError(f"{name}: HostPlan needs every buffer")
+            if t.device.type != "cpu":
+                raise ValueError(f"{name}: HostPlan takes host (CPU, ideally pinned) tensors")
+            if t.dtype != want or t.numel() != size[name] or not t.is_contiguous():
+                raise ValueError(f"{name}: expected a contiguous {want} tensor of {size[name]} elements, "
+                                 f"got {t.dtype} {tuple(t.shape)} contiguous={t.is_contiguous()}")
+        if info is not None and (info.device.type != "cpu" or info.dtype != torch.int32
+                                 or info.numel() != self.p.n_inst or not info.is_contiguous()):
+            raise ValueError(f"info: expected a contiguous CPU int32 tensor of {self.p.n_inst} elements")
         st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         with torch.cuda.device(self.device):
             _abi.check(_abi.load().smnn_plan_fwd_bwd_host(

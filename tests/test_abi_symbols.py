@@ -33,7 +33,7 @@ def test_header_symbols_exported(lib):
 def test_version_and_validation_without_gpu(lib):
     from paper_2410_06074_b200 import _abi
     assert b"sm_100a" in lib.smnn_version()
-    p = _abi.smnn_problem(n_inst=4, T=10, order=4, n_iv=1, dtype=0, threads_per_inst=0, reserved=0,
+    p = _abi.smnn_problem(n_inst=4, T=10, order=4, n_iv=1, dtype=0, threads_per_inst=0, path=0,
                           w_gov=1, w_init=1, w_smooth=1)
     rc = lib.smnn_factor_solve_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None)
     assert rc == -3 and b"order" in lib.smnn_last_error()
@@ -56,22 +56,59 @@ def test_product_path_refuses_cpu_tensors():
 
 
 def test_kernel_path_selection(lib):
-    """smnn_kernel_path (host logic only): fp32 -- the resident RF kernel for
-    instances that fit one CTA, the three-kernel pipeline for long horizons;
-    fp64 arithmetic -- the pipeline first; the checkpointing kernels when
-    neither fits."""
+    """smnn_kernel_path (host logic only): fp32 arithmetic -- the resident RF
+    kernel for instances that fit one CTA, the three-kernel pipeline for long
+    horizons; fp64 arithmetic -- the x64 cluster kernel while one cluster of
+    <= 16 CTAs holds the instance, then the pipeline; the checkpointing kernels
+    when none fits.  A forced path (smnn_problem.path) is taken when eligible."""
     import torch
     from paper_2410_06074_b200 import kernel_path
     assert kernel_path(1536, 1000, 2, 2) == "rf"                      # Lorenz (configs[1])
     assert kernel_path(1536, 1000, 2, 2, bwd=True) == "rf"
     assert kernel_path(4096, 1461, 2, 2) == "rf"                      # SST (configs[3])
-    assert kernel_path(4096, 10000, 2, 2) == "pipe"                   # north_star target
+    assert kernel_path(4096, 10000, 2, 2) == "pipe"                   # north_star target, fp32
     assert kernel_path(4096, 10000, 2, 2, bwd=True) == "pipe"
-    assert kernel_path(8192, 2000, 3, 3, compute="f64") == "pipe"     # KdV default (configs[2])
-    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "pipe"  # fp64: pipeline before rf
-    assert kernel_path(4096, 10000, 2, 2, dtype=torch.float64) == "pipe"  # 2048 separators: 8 per thread
+    assert kernel_path(8192, 2000, 3, 3, compute="f64") == "x64"      # KdV (configs[2])
+    assert kernel_path(4096, 10000, 2, 2, compute="f64") == "x64"     # north_star target, f32c64
+    assert kernel_path(4096, 10000, 2, 2, compute="f64", bwd=True) == "x64"
+    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "x64"
     assert kernel_path(64, 100000, 2, 2, dtype=torch.float64) == "checkpoint"  # > 2048 separators
     assert kernel_path(2, 3, 2, 2) == "checkpoint"                    # too short to chunk
+    assert kernel_path(1536, 1000, 2, 2, compute="f64", path="pipe") == "pipe"
+    assert kernel_path(1536, 1000, 2, 2, path="x64") == "rf"          # x64 needs fp64 arithmetic: fallback
+    assert kernel_path(1536, 1000, 2, 2, path="resident") == "checkpoint"
+
+
+def test_launch_count(lib):
+    """smnn_launch_count: one launch for rf / x64 / checkpoint, three for the
+    pipeline; an SMNN_F32_C64 backward on a path that reads y from storage runs
+    as SMNN_F64 on promoted copies (5 widenings, fp64 forward + backward,
+    4 narrowings, 1 info merge)."""
+    from paper_2410_06074_b200 import _abi
+
+    def count(T, dtype, bwd, path=0, n=64):
+        p = _abi.smnn_problem(n_inst=n, T=T, order=2, n_iv=2, dtype=dtype, threads_per_inst=0, path=path,
+                              w_gov=1, w_init=1, w_smooth=1)
+        return lib.smnn_launch_count(ctypes.byref(p), bwd)
+    assert count(1000, _abi.SMNN_F32, 0) == 1 and count(1000, _abi.SMNN_F32, 1) == 1
+    assert count(10000, _abi.SMNN_F32, 0) == 3
+    assert count(10000, _abi.SMNN_F32_C64, 1) == 1                       # x64 re-solves y itself
+    assert count(1000, _abi.SMNN_F32_C64, 1, path=_abi.SMNN_PATH_PIPE) == 5 + 3 + 3 + 4 + 1
+    assert count(100000, _abi.SMNN_F32_C64, 1) == 5 + 1 + 1 + 4 + 1      # checkpoint kernels, promoted
+
+
+def test_workspace_covers_promotion(lib):
+    """An SMNN_F32_C64 backward that is promoted to SMNN_F64 needs fp64 copies of
+    the inputs, dl/dy, y and the gradients (9 [n, T, b]-sized or smaller arrays)
+    plus the fp64 path's own workspace."""
+    from paper_2410_06074_b200 import _abi
+    n, T = 64, 100000
+    p = _abi.smnn_problem(n_inst=n, T=T, order=2, n_iv=2, dtype=_abi.SMNN_F32_C64, threads_per_inst=0, path=0,
+                          w_gov=1, w_init=1, w_smooth=1)
+    q = _abi.smnn_problem(n_inst=n, T=T, order=2, n_iv=2, dtype=_abi.SMNN_F64, threads_per_inst=0, path=0,
+                          w_gov=1, w_init=1, w_smooth=1)
+    need = 8 * n * T * (4 * 3 + 2 + 2) + lib.smnn_workspace_bytes(ctypes.byref(q))
+    assert lib.smnn_workspace_bytes(ctypes.byref(p)) >= need
 
 
 def test_workspace_covers_the_pipeline(lib):
@@ -82,7 +119,7 @@ def test_workspace_covers_the_pipeline(lib):
     register segments per chunk)."""
     from paper_2410_06074_b200 import _abi
     for dtype, es, K in ((_abi.SMNN_F32, 4, 1024), (_abi.SMNN_F64, 8, 1024)):
-        p = _abi.smnn_problem(n_inst=4096, T=10000, order=2, n_iv=2, dtype=dtype, threads_per_inst=0, reserved=0,
+        p = _abi.smnn_problem(n_inst=4096, T=10000, order=2, n_iv=2, dtype=dtype, threads_per_inst=0, path=0,
                               w_gov=1, w_init=1, w_smooth=1)
         need = 4096 * K * ((2 * 6 + 2 * 3 + 9) * es + 3 * es + 4)
         assert lib.smnn_workspace_bytes(ctypes.byref(p)) >= need
