@@ -47,7 +47,7 @@ __device__ __forceinline__ void rcopyL(const S (&src)[B][B], S (&dst)[B][B]) {
 #define SMNN_PIPE_HM4D 4  // fp64 arithmetic, order 3 (b = 4)
 #endif
 // P2 register segment: the factors of up to HM interior points stay in registers.
-template <int B, class S>
+template <int B, class S, int NR = 1>
 struct PipeHM {
   static constexpr int value = sizeof(S) >= 8 ? (B == 1 ? 12 : B == 2 ? 8 : B == 3 ? 5 : SMNN_PIPE_HM4D)
                                               : (B == 1 ? 23 : B == 2 ? 13 : B == 3 ? 9 : 6);
@@ -61,49 +61,79 @@ struct PipeCM {
   static constexpr int value = sizeof(S) >= 8 ? 2 * PipeHM<B, S>::value : PipeHM<B, S>::value + 1;
 };
 
+// Right-hand sides of point i of a chunk (NR of them): rhs 0 = dl/dy (BWD) or
+// beta, rhs 1 = beta (BWD with NR = 2: y re-solved in the arithmetic type);
+// beta_j = wg2 c_j d_j (+ wi2 u at t = 0).
+template <int B, class Tio, class S, bool BWD, int NR>
+__device__ __forceinline__ void chunk_rhs(const Wts<S>& w, int n_iv, const Tio* u, bool t0, const S (&wc)[B],
+                                          const Tio* dS, const Tio* gS, int i, S (&rhs)[NR][B]) {
+  static_assert(NR == 1 || (NR == 2 && BWD), "two right-hand sides only in the backward pass");
+  constexpr int qb = BWD ? 1 : 0;  // index of beta
+  if (BWD) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) rhs[0][r] = S(gS[i * B + r]);
+  }
+  if (qb < NR) {
+    const S d = S(dS[i]);
+#pragma unroll
+    for (int r = 0; r < B; ++r) rhs[qb < NR ? qb : 0][r] = mul_(wc[r], d);
+    if (t0) {
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+        if (r < n_iv) rhs[qb < NR ? qb : 0][r] = fma_(w.i2, S(u[r]), rhs[qb < NR ? qb : 0][r]);
+    }
+  }
+}
+
+// rhs -= P w (the Schur coupling of the right-hand side only)
+template <int B, class S>
+__device__ __forceinline__ void lcouple_v(const S (&P)[B][B], const S (&w)[B], S (&rhs)[B]) {
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    S acc = rhs[i];
+#pragma unroll
+    for (int j = 0; j < B; ++j) acc = fnma_(P[i][j], w[j], acc);
+    rhs[i] = acc;
+  }
+}
+
 // Pass 1 of one chunk (interior nint >= 1 points, then the separator): block
 // Cholesky of the interior with the spike (Algorithm 3's loop), the Schur
 // complement onto the two separators, the separator's own block.  Returns the
 // separator block Dsep (lower), rhs Rsep, coupling A_rl, and sum X^T X /
 // sum X^T w (to be negated into A_ll / r_l of separator k-1); true on a
-// pivot breakdown.  Shared by the pipeline's P1 and the fused rf2 kernel.
-template <int B, class Tio, class S, bool BWD, int CM>
+// pivot breakdown.  NR right-hand sides share the factorisation.
+template <int B, class Tio, class S, bool BWD, int CM, int NR = 1>
 __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u, int k, int K, int nint,
                                          const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS,
-                                         S (&Dsep)[B][B], S (&Rsep)[B], S (&Arl)[B][B], S (&All)[B][B],
-                                         S (&rl)[B]) {
+                                         S (&Dsep)[B][B], S (&Rsep)[NR][B], S (&Arl)[B][B], S (&All)[B][B],
+                                         S (&rl)[NR][B]) {
   S ap[2 * B - 1];
   if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
-  S Lc[B][B], wv[B], X[B][B];
-  zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
+  S Lc[B][B], wv[NR][B], X[B][B];
+  zero<B, S>(Lc); zero<B, S>(X); zero<B, S>(All);
+#pragma unroll
+  for (int q = 0; q < NR; ++q) { zero<B, S>(wv[q]); zero<B, S>(rl[q]); }
   S sg = splat<S>(1.0);
 #pragma unroll
   for (int i = 0; i < CM - 1; ++i) {
     if (i < nint) {
-      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
+      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[NR][B];
 #pragma unroll
       for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
       spow<B, S>(S(sS[i]), w.s2, an);
       lassemble<B, S>(c, w.g2, ap, an, M, wc);
-      if (BWD) {
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
-      } else {
-        const S d = S(dS[i]);
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
-      }
-      if (i == 0 && k == 0) {  // initial-value rows at t = 0
+      const bool t0 = i == 0 && k == 0;
+      chunk_rhs<B, Tio, S, BWD, NR>(w, n_iv, u, t0, wc, dS, gS, i, rhs);
+      if (t0) {  // initial-value rows at t = 0
 #pragma unroll
         for (int r = 0; r < B; ++r)
-          if (r < n_iv) {
-            if (!BWD) rhs[r] = fma_(w.i2, S(u[r]), rhs[r]);
-            M[r][r] = add_(M[r][r], w.i2);
-          }
+          if (r < n_iv) M[r][r] = add_(M[r][r], w.i2);
       }
       if (i == 0) {
         lchol<B, S>(M, Lc);
-        llsolve<B, S>(Lc, rhs, wv);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) llsolve<B, S>(Lc, rhs[q], wv[q]);
         S NL[B][B];  // spike X_f = L_f^{-1} N_{f-1} (zero for k = 0: ap = 0)
         lN<B, S>(ap, NL);
         lleft<B, S>(Lc, NL, X);
@@ -116,17 +146,23 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
             for (int m = 1; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
             All[r][q] = acc;
           }
-          S acc = mul_(X[0][r], wv[0]);
 #pragma unroll
-          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
-          rl[r] = acc;
+          for (int q = 0; q < NR; ++q) {
+            S acc = mul_(X[0][r], wv[q][0]);
+#pragma unroll
+            for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[q][m], acc);
+            rl[q][r] = acc;
+          }
         }
       } else {
         S Pm[B][B];
         lPfromN<B, S>(ap, Lc, Pm);  // P_{j-1} = N_{j-1} L_{j-1}^{-T}
-        lcouple<B, S>(Pm, wv, M, rhs);
+        lcouple<B, S>(Pm, wv[0], M, rhs[0]);
+#pragma unroll
+        for (int q = 1; q < NR; ++q) lcouple_v<B, S>(Pm, wv[q], rhs[q]);
         lchol<B, S>(M, Lc);
-        llsolve<B, S>(Lc, rhs, wv);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) llsolve<B, S>(Lc, rhs[q], wv[q]);
         S Y[B][B];  // spike X_j = -L_j^{-1} P_{j-1} X_{j-1}, carried with sign sg
 #pragma unroll
         for (int r = 0; r < B; ++r)
@@ -148,10 +184,13 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
             for (int m = 0; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
             All[r][q] = acc;
           }
-          S acc = mul_(X[0][r], wv[0]);
 #pragma unroll
-          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[m], acc);
-          rl[r] = fma_(sg, acc, rl[r]);
+          for (int q = 0; q < NR; ++q) {
+            S acc = mul_(X[0][r], wv[q][0]);
+#pragma unroll
+            for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[q][m], acc);
+            rl[q][r] = fma_(sg, acc, rl[q][r]);
+          }
         }
       }
 #pragma unroll
@@ -177,15 +216,10 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
     for (int r = 0; r < B; ++r) c[r] = S(cS[nint * B + r]);
     if (k + 1 < K) spow<B, S>(S(sS[nint]), w.s2, an); else zero<2 * B - 1, S>(an);
     lassemble<B, S>(c, w.g2, ap, an, Dsep, wc);
-    if (BWD) {
+    chunk_rhs<B, Tio, S, BWD, NR>(w, n_iv, u, false, wc, dS, gS, nint, Rsep);
+    lcouple<B, S>(Pl, wv[0], Dsep, Rsep[0]);
 #pragma unroll
-      for (int r = 0; r < B; ++r) Rsep[r] = S(gS[nint * B + r]);
-    } else {
-      const S d = S(dS[nint]);
-#pragma unroll
-      for (int r = 0; r < B; ++r) Rsep[r] = mul_(wc[r], d);
-    }
-    lcouple<B, S>(Pl, wv, Dsep, Rsep);
+    for (int q = 1; q < NR; ++q) lcouple_v<B, S>(Pl, wv[q], Rsep[q]);
   }
   return bad;
 }
@@ -193,62 +227,63 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
 // One segment [i0, i0 + len) of a chunk interior (len <= HM) in pass 2: forward
 // sweep re-factoring M from the state (Ls, ws) = (L, w') at step i0 - 1 (from
 // the chunk start -- initial-value rows, rhs -= N_{f-1} y_L -- when i0 == 0),
-// then, if STORE, back substitution from (yn, yfn) = (y, y_fwd) at step
-// i0 + len, writing the outputs and returning (yn, yfn) at step i0.  Without
-// STORE the sweep only runs through and returns the state at the last step.
-template <int B, class Tio, class S, bool BWD, int HM, bool STORE>
+// then, if STORE, back substitution from yn = y at step i0 + len (NR = 2
+// backward: yn[0] = lambda, yn[1] = y re-solved; NR = 1 backward: y_fwd read
+// from storage into yfn), writing the outputs and returning yn at step i0.
+// Without STORE the sweep only runs through and returns the state at the last step.
+template <int B, class Tio, class S, bool BWD, int HM, bool STORE, int NR>
 __device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, int k, int f, int i0, int len,
                                        const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS, Tio* wS,
-                                       const S (&yL)[B], S (&Ls)[B][B], S (&ws)[B], S (&yn)[B], S (&yfn)[B]) {
-  constexpr bool WSM = sizeof(S) == sizeof(Tio);
+                                       const S (&yL)[NR][B], S (&Ls)[B][B], S (&ws)[NR][B], S (&yn)[NR][B],
+                                       S (&yfn)[B]) {
+  constexpr bool WSM = sizeof(S) == sizeof(Tio) && NR == 1;
   S Lr[STORE ? HM : 1][B][B];
-  S Wp[(STORE && !WSM) ? HM : 1][B];
+  S Wp[(STORE && !WSM) ? HM : 1][NR][B];
   S ap[2 * B - 1];
   if (i0 > 0 || k > 0) spow<B, S>(S(sS[i0 - 1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
 #pragma unroll
   for (int q = 0; q < HM; ++q) {
     if (q < len) {
       const int i = i0 + q;
-      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[B];
+      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[NR][B];
 #pragma unroll
       for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
       spow<B, S>(S(sS[i]), w.s2, an);
       lassemble<B, S>(c, w.g2, ap, an, M, wc);
-      if (BWD) {
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = S(gS[i * B + r]);
-      } else {
-        const S d = S(dS[i]);
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = mul_(wc[r], d);
-      }
+      const bool t0 = i == 0 && k == 0;
+      chunk_rhs<B, Tio, S, BWD, NR>(w, x.n_iv, x.u[0], t0, wc, dS, gS, i, rhs);
       if (i == 0) {  // chunk start (q == 0, i0 == 0)
-        if (k == 0) {
+        if (t0) {
 #pragma unroll
           for (int r = 0; r < B; ++r)
-            if (r < x.n_iv) {
-              if (!BWD) rhs[r] = fma_(w.i2, S(x.u[0][r]), rhs[r]);
-              M[r][r] = add_(M[r][r], w.i2);
-            }
+            if (r < x.n_iv) M[r][r] = add_(M[r][r], w.i2);
         }
-        S Nt[B];  // rhs -= N_{f-1} y_L
-        rNv<B, S>(ap, yL, Nt);
 #pragma unroll
-        for (int r = 0; r < B; ++r) rhs[r] = sub_(rhs[r], Nt[r]);
+        for (int p = 0; p < NR; ++p) {  // rhs -= N_{f-1} y_L
+          S Nt[B];
+          rNv<B, S>(ap, yL[p], Nt);
+#pragma unroll
+          for (int r = 0; r < B; ++r) rhs[p][r] = sub_(rhs[p][r], Nt[r]);
+        }
       } else {
         S Pm[B][B];
         lPfromN<B, S>(ap, (STORE && q > 0) ? Lr[STORE ? (q > 0 ? q - 1 : 0) : 0] : Ls, Pm);
-        lcouple<B, S>(Pm, ws, M, rhs);
+        lcouple<B, S>(Pm, ws[0], M, rhs[0]);
+#pragma unroll
+        for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pm, ws[p], rhs[p]);
       }
       S Lc[B][B];
       lchol<B, S>(M, Lc);
-      llsolve<B, S>(Lc, rhs, ws);
+#pragma unroll
+      for (int p = 0; p < NR; ++p) llsolve<B, S>(Lc, rhs[p], ws[p]);
       if (STORE) {
         rcopyL<B, S>(Lc, Lr[STORE ? q : 0]);
 #pragma unroll
-        for (int r = 0; r < B; ++r) {
-          if (WSM) wS[i * B + r] = Tio(ws[r]); else Wp[(STORE && !WSM) ? q : 0][r] = ws[r];
-        }
+        for (int p = 0; p < NR; ++p)
+#pragma unroll
+          for (int r = 0; r < B; ++r) {
+            if (WSM) wS[i * B + r] = Tio(ws[p][r]); else Wp[(STORE && !WSM) ? q : 0][p][r] = ws[p][r];
+          }
       } else {
         rcopyL<B, S>(Lc, Ls);
       }
@@ -261,92 +296,120 @@ __device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, in
   for (int q = HM - 1; q >= 0; --q) {
     if (q < len) {
       const int i = i0 + q, j = f + i;
-      S an[2 * B - 1], v[B], uu[B], t[B], yv[B];
+      S an[2 * B - 1], yv[NR][B];
       spow<B, S>(S(sS[i]), w.s2, an);
-      rNtv<B, S>(an, yn, v);
-      llsolve<B, S>(Lr[STORE ? q : 0], v, uu);
 #pragma unroll
-      for (int r = 0; r < B; ++r) t[r] = sub_(WSM ? S(wS[i * B + r]) : Wp[(STORE && !WSM) ? q : 0][r], uu[r]);
-      lltsolve<B, S>(Lr[STORE ? q : 0], t, yv);
+      for (int p = 0; p < NR; ++p) {
+        S v[B], uu[B], t[B];
+        rNtv<B, S>(an, yn[p], v);
+        llsolve<B, S>(Lr[STORE ? q : 0], v, uu);
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+          t[r] = sub_(WSM ? S(wS[i * B + r]) : Wp[(STORE && !WSM) ? q : 0][p][r], uu[r]);
+        lltsolve<B, S>(Lr[STORE ? q : 0], t, yv[p]);
+      }
       if (!BWD) {
 #pragma unroll
-        for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[r]);
+        for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[0][r]);
       } else {
-        S yf[B];
-        ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
-        lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv, yf);
-        if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv, yf, yn, yfn));
+        S yf[B];  // y at j: re-solved (NR = 2) or read from storage
+        if (NR == 2) {
+#pragma unroll
+          for (int r = 0; r < B; ++r) yf[r] = yv[NR - 1][r];
+        } else {
+          ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
+        }
+        lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv[0], yf);
+        if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv[0], yf, yn[0], yfn));
 #pragma unroll
         for (int r = 0; r < B; ++r) yfn[r] = yf[r];
       }
 #pragma unroll
-      for (int r = 0; r < B; ++r) yn[r] = yv[r];
+      for (int p = 0; p < NR; ++p)
+#pragma unroll
+        for (int r = 0; r < B; ++r) yn[p][r] = yv[p][r];
     }
   }
 }
 
-// Pass 2 of one chunk with y_L = y(sigma_{k-1}) and y_R = y(sigma_k) known:
-// outputs at the separator, then the interior in (at most) two register
-// segments (p2_seg).  Shared by the pipeline's P2 and the fused rf2 kernel.
-template <int B, class Tio, class S, bool BWD, int CM>
+// Pass 2 of one chunk with y_L = y(sigma_{k-1}) and y_R = y(sigma_k) known
+// (NR right-hand sides): outputs at the separator, then the interior in (at
+// most) two register segments (p2_seg).
+template <int B, class Tio, class S, bool BWD, int CM, int NR = 1>
 __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, int k, int f, int sig, int nint,
                                          const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS,
-                                         const S (&yL)[B], const S (&yR)[B]) {
-    // outputs at the separator, then the interior in (at most) two register
-  // segments: a chunk longer than HM is split as [0, h) + [h, nint) with the
-  // second segment HM long; [0, h) is factored twice (run-through to reach
-  // the state at h - 1, then stored for its back substitution).
-  constexpr int HM = PipeHM<B, S>::value;
+                                         const S (&yL)[NR][B], const S (&yR)[NR][B]) {
+  // a chunk longer than HM is split as [0, h) + [h, nint) with the second
+  // segment HM long; [0, h) is factored twice (run-through to reach the state
+  // at h - 1, then stored for its back substitution).
+  constexpr int HM = PipeHM<B, S, NR>::value;
   static_assert(CM - 1 <= 2 * HM, "two segments must cover a chunk");
   Tio* wS = const_cast<Tio*>(BWD ? gS : cS);
-  S yn[B], yfn[B], Ls[B][B], ws[B];
+  S yn[NR][B], yfn[B], Ls[B][B], ws[NR][B];
 #pragma unroll
-  for (int r = 0; r < B; ++r) yn[r] = yR[r];
+  for (int p = 0; p < NR; ++p) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) yn[p][r] = yR[p][r];
+    zero<B, S>(ws[p]);
+  }
   zero<B, S>(yfn);
   zero<B, S>(Ls);
-  zero<B, S>(ws);
   if (!BWD) {
 #pragma unroll
-    for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, sig * B + r, yR[r]);
+    for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, sig * B + r, yR[0][r]);
   } else {
-    ldlv<B, S, Tio, 1, true>(x.yin, sig * B, yfn);
-    lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR, yfn);
+    if (NR == 2) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) yfn[r] = yR[NR - 1][r];
+    } else {
+      ldlv<B, S, Tio, 1, true>(x.yin, sig * B, yfn);
+    }
+    lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR[0], yfn);
   }
   if (CM - 1 <= HM || nint <= HM) {
-    p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, 0, nint, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+    p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, 0, nint, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
   } else {
     const int h = nint - HM;
-    p2_seg<B, Tio, S, BWD, HM, false>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
-    p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, h, HM, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+    p2_seg<B, Tio, S, BWD, HM, false, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+    p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, h, HM, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
     zero<B, S>(Ls);
-    zero<B, S>(ws);
-    p2_seg<B, Tio, S, BWD, HM, true>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+#pragma unroll
+    for (int p = 0; p < NR; ++p) zero<B, S>(ws[p]);
+    p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
   }
   if (BWD && k > 0 && x.gs.on) {  // interval (sigma_{k-1}, f)
     S yfm[B], am[2 * B - 1];
-    ldlv<B, S, Tio, 1, true>(x.yin, (f - 1) * B, yfm);
+    if (NR == 2) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) yfm[r] = yL[NR - 1][r];
+    } else {
+      ldlv<B, S, Tio, 1, true>(x.yin, (f - 1) * B, yfm);
+    }
     spow<B, S>(S(sS[-1]), w.s2, am);
-    stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL, yfm, yn, yfn));
+    stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL[0], yfm, yn[0], yfn));
   }
 }
 
-template <int B>
-struct PSep {
+template <int B, int NR = 1>
+struct PSep {  // workspace record of one separator (field-major over the separators)
   static constexpr int LT = B * (B + 1) / 2;
-  static constexpr int D = 0, R = LT, BL = LT + B, AL = LT + B + B * B, RL = 2 * LT + B + B * B;
-  static constexpr int N = 2 * LT + 2 * B + B * B;
+  static constexpr int D = 0, R = LT, BL = LT + NR * B, AL = LT + NR * B + B * B, RL = 2 * LT + NR * B + B * B;
+  static constexpr int N = 2 * LT + 2 * NR * B + B * B;
 };
 
-template <int B, class S>
-__device__ __forceinline__ void psep_ld(const S* in, int K, int NT, int j, S (&D)[B][B], S (&r)[B], S (&Bl)[B][B]) {
-  using Q = PSep<B>;
+template <int B, class S, int NR = 1>
+__device__ __forceinline__ void psep_ld(const S* in, int K, int NT, int j, S (&D)[B][B], S (&r)[NR][B],
+                                        S (&Bl)[B][B]) {
+  using Q = PSep<B, NR>;
   int e = 0;
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
     for (int q = 0; q <= i; ++q) D[i][q] = in[int64_t(Q::D + e++) * K + j];
 #pragma unroll
-  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + j];
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int i = 0; i < B; ++i) r[p][i] = in[int64_t(Q::R + p * B + i) * K + j];
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
@@ -358,27 +421,33 @@ __device__ __forceinline__ void psep_ld(const S* in, int K, int NT, int j, S (&D
 #pragma unroll
       for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], in[int64_t(Q::AL + e++) * K + j + 1]);
 #pragma unroll
-    for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + j + 1]);
+    for (int p = 0; p < NR; ++p)
+#pragma unroll
+      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], in[int64_t(Q::RL + p * B + i) * K + j + 1]);
   }
 }
 
-template <int B, class S>
-__device__ __forceinline__ void psep_ld_rb(const S* in, int K, int NT, int j, S (&r)[B], S (&Bl)[B][B]) {
-  using Q = PSep<B>;
+template <int B, class S, int NR = 1>
+__device__ __forceinline__ void psep_ld_rb(const S* in, int K, int NT, int j, S (&r)[NR][B], S (&Bl)[B][B]) {
+  using Q = PSep<B, NR>;
 #pragma unroll
-  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + j];
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int i = 0; i < B; ++i) r[p][i] = in[int64_t(Q::R + p * B + i) * K + j];
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
     for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
   if (j + 1 < K && (j + 1) % NT == 0) {
 #pragma unroll
-    for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + j + 1]);
+    for (int p = 0; p < NR; ++p)
+#pragma unroll
+      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], in[int64_t(Q::RL + p * B + i) * K + j + 1]);
   }
 }
-template <int B, class S>
+template <int B, class S, int NR = 1>
 __device__ __forceinline__ void psep_ld_b(const S* in, int K, int j, S (&Bl)[B][B]) {
-  using Q = PSep<B>;
+  using Q = PSep<B, NR>;
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll

@@ -365,37 +365,34 @@ int64_t n_groups(const smnn_problem* p) {
   return (p->n_inst + P - 1) / P;
 }
 
-int device_sms() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    sms = v;
-  }
-  return sms;
+int device_sms() {  // of the current device
+  int dev = 0, v = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    return v;
+  cudaGetLastError();
+  return 148;
 }
 
-// Occupancy of a kernel (cached per kernel / block / smem).
+// Occupancy of a kernel (cached per device / kernel / block / smem); raises
+// the kernel's dynamic shared-memory limit on this device (ensure_smem).
 std::mutex g_occ_mu;
-std::map<std::tuple<const void*, int, size_t>, int> g_occ;
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
 
 template <class Kern>
 int occupancy(Kern kernel, int nt, size_t smem) {
-  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), nt, smem);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kernel), nt, smem);
+  smnn::ensure_smem(reinterpret_cast<const void*>(kernel), smem);
   {
     std::lock_guard<std::mutex> lk(g_occ_mu);
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
   }
   int occ = 1;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, smem);
-  {  // keep the attribute at the largest request (a smaller one may have lowered it)
-    static std::map<const void*, size_t> top;
-    std::lock_guard<std::mutex> lk(g_occ_mu);
-    size_t& t = top[reinterpret_cast<const void*>(kernel)];
-    t = std::max(t, smem);
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(t));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, smem) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 1;
   }
   occ = std::max(occ, 1);
   std::lock_guard<std::mutex> lk(g_occ_mu);
@@ -440,11 +437,15 @@ int kernel_path(const smnn_problem* p, bool bwd);
 // ---- SMNN_F32_C64 backward on the paths that read y from storage --------
 // The gradients' residual terms (d - c.y, the Taylor-row residuals) amplify
 // the fp32 rounding of y by up to ~1e4, so an fp32-stored y cannot give 1e-4
-// gradients.  The x64 kernel re-solves y in fp64 beside dl/dbeta; every other
-// path runs the backward as SMNN_F64 on promoted copies instead: inputs and
+// gradients.  The x64 kernel and the pipeline re-solve y in fp64 beside
+// dl/dbeta (two right-hand sides, one factorisation); the other paths run the backward as SMNN_F64 on promoted copies instead: inputs and
 // dl/dy widened to fp64 in the workspace, the fp64 forward (y in fp64), the
 // fp64 backward, gradients narrowed into the caller's fp32 outputs.
-bool promote_bwd(const smnn_problem* p) { return p->dtype == SMNN_F32_C64 && kernel_path(p, true) != SMNN_PATH_X64; }
+bool promote_bwd(const smnn_problem* p) {
+  if (p->dtype != SMNN_F32_C64) return false;
+  const int path = kernel_path(p, true);
+  return path != SMNN_PATH_X64 && path != SMNN_PATH_PIPE;  // both re-solve y in fp64 themselves
+}
 
 smnn_problem as_f64(const smnn_problem* p) {
   smnn_problem q = *p;
@@ -563,8 +564,9 @@ int launch_resident(const smnn_problem* p, const smnn::Args<Tio>& a, const RPlan
   using S = typename smnn::LaneOf<Tio, Tc>::S;
   auto kern = rp.L.cs > 1 ? smnn::resident_kernel<B, Tio, S, BWD, smnn::SegLen<B, S>::value, true>
                           : smnn::resident_kernel<B, Tio, S, BWD, smnn::SegLen<B, S>::value, false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rp.smem));
-  if (rp.L.cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (const int e0 = check_cuda(smnn::ensure_smem(reinterpret_cast<const void*>(kern), rp.smem),
+                                "resident kernel shared-memory attribute"))
+    return e0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -579,8 +581,10 @@ int launch_resident(const smnn_problem* p, const smnn::Args<Tio>& a, const RPlan
   cfg.gridDim = dim3(rp.L.cs);
   int nclusters = 0;
   static std::mutex mu;
-  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
-  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), rp.L.cs, rp.L.nt, rp.smem);
+  static std::map<std::tuple<int, const void*, int, int, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kern), rp.L.cs, rp.L.nt, rp.smem);
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);

@@ -28,9 +28,14 @@ struct PipePlan {
   PipeL L1{}, L2{};
 };
 
+// Right-hand sides of a pipeline call: 2 in the SMNN_F32_C64 backward (dl/dy and
+// beta: y is re-solved in fp64 beside lambda; see include/smnn.h smnn_solve_bwd).
+int pipe_nr(const smnn_problem* p, bool bwd) { return (bwd && p->dtype == SMNN_F32_C64) ? 2 : 1; }
+
 template <int B, class S>
 PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
   PipePlan q;
+  const int nr = pipe_nr(p, bwd);
   constexpr int CM = PipeCM<B, S>::value;
   const int T = p->T;
   if (p->threads_per_inst != 0 || T < 4) return q;
@@ -57,11 +62,11 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     size_t off = 0;
     auto take = [&](size_t bytes) { const size_t o = off; off = al16(off + bytes); return int(o); };
     L.off_c = take(size_t(steps) * B * es + 32);
-    L.off_d = (p2 || !bwd) ? take(size_t(steps) * es + 32) : 0;
+    L.off_d = (p2 || !bwd || nr == 2) ? take(size_t(steps) * es + 32) : 0;
     L.off_s = take(size_t(steps) * es + 32);
     L.off_g = bwd ? take(size_t(steps) * B * es + 32) : 0;
-    L.off_y = (bwd && p2) ? take(size_t(steps) * B * es + 32) : 0;
-    L.off_h = p2 ? 0 : take(size_t(PSep<B>::LT + B) * SMNN_PIPE_NT * ls);
+    L.off_y = (bwd && p2 && nr == 1) ? take(size_t(steps) * B * es + 32) : 0;
+    L.off_h = p2 ? 0 : take(size_t(PSep<B>::LT + nr * B) * SMNN_PIPE_NT * ls);
     L.off_bar = take(16);
     return off;
   };
@@ -76,10 +81,11 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     q.NT /= 2;
   }
   q.parts = (K + q.NT - 1) / q.NT;
-  q.smem_sep = size_t(BRec<B>::N) * (q.sep2 ? K / q.m2 : K) * ls + size_t(2 * K + 4) * 4;
+  const size_t recn = nr == 2 ? size_t(BRecN<B, 2>::N) : size_t(BRecN<B, 1>::N);
+  q.smem_sep = recn * (q.sep2 ? K / q.m2 : K) * ls + size_t(2 * K + 4) * 4;
   if (q.smem_p1 > 200 * 1024 || q.smem_p2 > 200 * 1024 || q.smem_sep > 220 * 1024) return q;
-  q.ws_sep1 = al256(size_t(p->n_inst) * PSep<B>::N * K * ls);
-  q.ws_ysep = al256(size_t(p->n_inst) * B * K * ls);
+  q.ws_sep1 = al256(size_t(p->n_inst) * (nr == 2 ? PSep<B, 2>::N : PSep<B, 1>::N) * K * ls);
+  q.ws_ysep = al256(size_t(p->n_inst) * nr * B * K * ls);
   q.ws_fail = al256(size_t(p->n_inst) * K * 4);
   for (PipeL* L : {&q.L1, &q.L2}) {
     L->K = K;
@@ -105,15 +111,15 @@ PipePlan plan_of(const smnn_problem* p, bool bwd) {
   return plan_S<double>(p, p->dtype == SMNN_F64 ? 8 : 4, bwd);
 }
 
-template <int B, class Tio, class S, bool BWD>
+template <int B, class Tio, class S, bool BWD, int NR>
 int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
   constexpr int CM = PipeCM<B, S>::value;
   PipePlan q = plan_B<B, S>(p, sizeof(Tio), BWD);
   if (!q.ok) return 0;
-  auto k1 = pipe_p1_kernel<B, Tio, S, BWD, CM>;
-  auto k2 = pipe_sep_kernel<B, S>;
-  auto k2b = q.m2 > 4 ? pipe_sep2_kernel<B, S, 8> : pipe_sep2_kernel<B, S, 4>;
-  auto k3 = pipe_p2_kernel<B, Tio, S, BWD, CM>;
+  auto k1 = pipe_p1_kernel<B, Tio, S, BWD, CM, NR>;
+  auto k2 = pipe_sep_kernel<B, S, NR>;
+  auto k2b = q.m2 > 4 ? pipe_sep2_kernel<B, S, 8, NR> : pipe_sep2_kernel<B, S, 4, NR>;
+  auto k3 = pipe_p2_kernel<B, Tio, S, BWD, CM, NR>;
   for (auto [kp, sm] : {std::make_pair(reinterpret_cast<const void*>(k1), q.smem_p1),
                          std::make_pair(reinterpret_cast<const void*>(k3), q.smem_p2),
                          std::make_pair(q.sep2 ? reinterpret_cast<const void*>(k2b) : reinterpret_cast<const void*>(k2),
@@ -147,13 +153,22 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   return 1;
 }
 
+template <class Tio, class S, bool BWD, int NR>
+int launch_order_nr(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
+  switch (p->order) {
+    case 0: return launch_B<1, Tio, S, BWD, NR>(p, a, st, err);
+    case 1: return launch_B<2, Tio, S, BWD, NR>(p, a, st, err);
+    case 2: return launch_B<3, Tio, S, BWD, NR>(p, a, st, err);
+    default: return launch_B<4, Tio, S, BWD, NR>(p, a, st, err);
+  }
+}
+
 template <class Tio, class S, bool BWD>
 int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
-  switch (p->order) {
-    case 0: return launch_B<1, Tio, S, BWD>(p, a, st, err);
-    case 1: return launch_B<2, Tio, S, BWD>(p, a, st, err);
-    case 2: return launch_B<3, Tio, S, BWD>(p, a, st, err);
-    default: return launch_B<4, Tio, S, BWD>(p, a, st, err);
+  if constexpr (BWD && sizeof(S) > sizeof(Tio)) {  // SMNN_F32_C64 backward: y re-solved
+    return launch_order_nr<Tio, S, BWD, 2>(p, a, st, err);
+  } else {
+    return launch_order_nr<Tio, S, BWD, 1>(p, a, st, err);
   }
 }
 

@@ -22,8 +22,10 @@
 // Workspace (S = arithmetic type), per instance g and chunk / separator k,
 // field-major so that a warp's 32 consecutive chunks touch 128 contiguous
 // bytes per field:
-//   sep1 [g][PSep<B>::N][K]  D_own (lower, packed), R_own, A_rl, A_ll (packed), r_l
-//   ysep [g][B][K]           y at the separators
+//   sep1 [g][PSep<B,NR>::N][K]  D_own (lower, packed), R_own, A_rl, A_ll (packed), r_l
+//   ysep [g][NR B][K]           y at the separators (per right-hand side)
+// NR = 2 in the SMNN_F32_C64 backward: dl/dy and beta share the factorisation,
+// so y is re-solved in fp64 beside lambda instead of read from fp32 storage.
 //   cfail[g][K]              1 + first point of a chunk whose pivots broke down, else INT_MAX
 #pragma once
 
@@ -90,9 +92,9 @@ struct PRange {
 };
 
 // ============================================================== P1 ========
-template <int B, class Tio, class S, bool BWD, int CM>
+template <int B, class Tio, class S, bool BWD, int CM, int NR>
 __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MINB64 : 4) pipe_p1_kernel(Args<Tio> a, PipeL L) {
-  using Q = PSep<B>;
+  using Q = PSep<B, NR>;
   unsigned char* sm = smnn_dyn_smem;
   Tio* smT = reinterpret_cast<Tio*>(sm);
   const int T = a.T, K = L.K, tid = threadIdx.x;
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MI
   const Wts<S> w{opaque(splat<S>(a.wg2)), opaque(splat<S>(a.wi2)), opaque(splat<S>(a.ws2))};
   const int64_t tb = g * int64_t(T) * B, t1b = g * int64_t(T), tsb = g * int64_t(T - 1);
   const Span<Tio> pc(a.coeffs + tb + R.ta * B, (R.tb - R.ta) * B);
-  const Span<Tio> pd(a.rhs + t1b + R.ta, BWD ? 0 : R.tb - R.ta);
+  const Span<Tio> pd(a.rhs + t1b + R.ta, (BWD && NR == 1) ? 0 : R.tb - R.ta);
   const Span<Tio> ps(a.steps + tsb + R.slo, R.shi - R.slo);
   const Span<Tio> pg(BWD ? a.grad_y + tb + R.ta * B : a.coeffs, BWD ? (R.tb - R.ta) * B : 0);
   if (tid == 0) {
@@ -127,15 +129,14 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MI
   __syncthreads();  // barrier initialised
   mbar_wait(bar, 0);
 
-  S Dsep[B][B], Rsep[B], Arl[B][B], All[B][B], rl[B];
+  S Dsep[B][B], Rsep[NR][B], Arl[B][B], All[B][B], rl[NR][B];
   bool bad = false;
-  if (act) bad = p1_chunk<B, Tio, S, BWD, CM>(w, a.n_iv, u, k, K, nint, cS, dS, sS, gS, Dsep, Rsep, Arl, All, rl);
+  if (act) bad = p1_chunk<B, Tio, S, BWD, CM, NR>(w, a.n_iv, u, k, K, nint, cS, dS, sS, gS, Dsep, Rsep, Arl, All, rl);
   // A_ll = -sum X^T X, r_l = -sum X^T w belong to separator k - 1: hand them to
   // the left neighbour through shared memory (the staged inputs are still in
   // use, so a region of its own); a CTA's first chunk writes them to the
   // workspace for the previous CTA's last separator.
-  S* ho = reinterpret_cast<S*>(sm + L.off_h);
-  constexpr int HN = Q::LT + B;
+  S* ho = reinterpret_cast<S*>(sm + L.off_h);  // (LT + NR B) values per thread, field-major
   if (act) {
     int e = 0;
 #pragma unroll
@@ -143,7 +144,9 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MI
 #pragma unroll
       for (int q = 0; q <= r; ++q) ho[(e++) * SMNN_PIPE_NT + tid] = neg_(All[r][q]);
 #pragma unroll
-    for (int r = 0; r < B; ++r) ho[(Q::LT + r) * SMNN_PIPE_NT + tid] = neg_(rl[r]);
+    for (int p = 0; p < NR; ++p)
+#pragma unroll
+      for (int r = 0; r < B; ++r) ho[(Q::LT + p * B + r) * SMNN_PIPE_NT + tid] = neg_(rl[p][r]);
   }
   __syncthreads();
   if (!act) return;
@@ -154,9 +157,10 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MI
 #pragma unroll
       for (int q = 0; q <= r; ++q) Dsep[r][q] = add_(Dsep[r][q], ho[(e++) * SMNN_PIPE_NT + tid + 1]);
 #pragma unroll
-    for (int r = 0; r < B; ++r) Rsep[r] = add_(Rsep[r], ho[(Q::LT + r) * SMNN_PIPE_NT + tid + 1]);
+    for (int p = 0; p < NR; ++p)
+#pragma unroll
+      for (int r = 0; r < B; ++r) Rsep[p][r] = add_(Rsep[p][r], ho[(Q::LT + p * B + r) * SMNN_PIPE_NT + tid + 1]);
   }
-  (void)HN;
   // write the separator blocks (field-major: coalesced across the warp)
   S* o = reinterpret_cast<S*>(L.sep1) + g * int64_t(Q::N) * K + k;
   int e = 0;
@@ -165,31 +169,32 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MI
 #pragma unroll
     for (int q = 0; q <= r; ++q) o[int64_t(Q::D + e++) * K] = Dsep[r][q];
 #pragma unroll
-  for (int r = 0; r < B; ++r) o[int64_t(Q::R + r) * K] = Rsep[r];
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int r = 0; r < B; ++r) o[int64_t(Q::R + p * B + r) * K] = Rsep[p][r];
 #pragma unroll
   for (int r = 0; r < B; ++r)
 #pragma unroll
     for (int q = 0; q < B; ++q) o[int64_t(Q::BL + r * B + q) * K] = Arl[r][q];
-  if (tid == 0 && k > 0) {  // the previous CTA's last separator adds these (psep_nb)
+  if (tid == 0 && k > 0) {  // the previous CTA's last separator adds these (psep_ld)
     e = 0;
 #pragma unroll
     for (int r = 0; r < B; ++r)
 #pragma unroll
       for (int q = 0; q <= r; ++q) o[int64_t(Q::AL + e++) * K] = neg_(All[r][q]);
 #pragma unroll
-    for (int r = 0; r < B; ++r) o[int64_t(Q::RL + r) * K] = neg_(rl[r]);
+    for (int p = 0; p < NR; ++p)
+#pragma unroll
+      for (int r = 0; r < B; ++r) o[int64_t(Q::RL + p * B + r) * K] = neg_(rl[p][r]);
   }
   L.cfail[g * K + k] = bad ? f + 1 : INT_MAX;  // 1 + first point of the chunk
 }
 
 // ============================================================== SEP =======
-template <int B, class S>
+template <int B, class S, int NR>
 __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_t* info) {  // K <= 256 (larger K: sep2)
-  using Q = PSep<B>;
-  using BR = BRec<B>;
+  using BR = BRecN<B, NR>;
   unsigned char* sm = smnn_dyn_smem;
-  // threads ordered by the level at which their separator is eliminated
-  // (rf_chunk_of_thread): each reduction level runs on as few warps as possible
   const int K = L.K, k = int(threadIdx.x);
   const int64_t g = blockIdx.x;
   S* rec = reinterpret_cast<S*>(sm);
@@ -197,43 +202,26 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
   int* sfail = stime + K;
   if (k == 0) sfail[0] = INT_MAX;
   stime[k] = chunk_begin(k + 1, T, K) - 1;
-  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(Q::N) * K;
-  S D[B][B], Bl[B][B], Cr[B][B], r[B];
-  int e = 0;
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int q = 0; q <= i; ++q) D[i][q] = in[int64_t(Q::D + e++) * K + k];
-#pragma unroll
-  for (int i = 0; i < B; ++i) r[i] = in[int64_t(Q::R + i) * K + k];
-#pragma unroll
-  for (int i = 0; i < B; ++i)
-#pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + k];
-  if (k + 1 < K) {  // the coupling to sigma_{k+1} (and A_ll, r_l across a P1 CTA boundary)
-    if ((k + 1) % L.NT == 0) {
-      e = 0;
-#pragma unroll
-      for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], in[int64_t(Q::AL + e++) * K + k + 1]);
-#pragma unroll
-      for (int i = 0; i < B; ++i) r[i] = add_(r[i], in[int64_t(Q::RL + i) * K + k + 1]);
-    }
+  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B, NR>::N) * K;
+  S D[B][B], Bl[B][B], Cr[B][B], r[NR][B];
+  psep_ld<B, S, NR>(in, K, L.NT, k, D, r, Bl);  // own block + A_ll, r_l across a P1 CTA boundary
+  if (k + 1 < K) {  // the coupling to sigma_{k+1}
+    S Bn[B][B];
+    psep_ld_b<B, S, NR>(in, K, k + 1, Bn);
 #pragma unroll
     for (int i = 0; i < B; ++i)
 #pragma unroll
-      for (int q = 0; q < B; ++q) Cr[i][q] = in[int64_t(Q::BL + q * B + i) * K + k + 1];
+      for (int q = 0; q < B; ++q) Cr[i][q] = Bn[q][i];
   } else {
     zero<B, S>(Cr);
   }
   const int cf = L.cfail[g * K + k];
   __syncthreads();
   if (cf != INT_MAX) atomicMin(sfail, cf);
-  rbcr2<B, S>(rec, K, k, stime, sfail, D, Bl, Cr, r);
-  S* y = reinterpret_cast<S*>(L.ysep) + g * int64_t(B) * K + k;
+  rbcr2n<B, S, NR>(rec, K, k, stime, sfail, D, Bl, Cr, r);
+  S* y = reinterpret_cast<S*>(L.ysep) + g * int64_t(NR * B) * K + k;
 #pragma unroll
-  for (int i = 0; i < B; ++i) y[int64_t(i) * K] = rec[k * BR::N + BR::Y + i];
+  for (int i = 0; i < NR * B; ++i) y[int64_t(i) * K] = rec[k * BR::N + BR::Y + i];
   if (k == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
 }
 
@@ -246,12 +234,11 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
 // the first m - 1 (with the spike towards super-separator t - 1, factors kept
 // in registers), the K/m super-separators j0 + m - 1 are solved by rbcr2, and
 // the owned separators are recovered by forward + back substitution.
-template <int B, class S, int MS>
+template <int B, class S, int MS, int NR>
 __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
-  using BR = BRec<B>;
+  using BR = BRecN<B, NR>;
   unsigned char* sm = smnn_dyn_smem;
   const int K = L.K, nt = blockDim.x;
-  // super-separator of this thread: identity, or grouped by reduction level
   const int t = int(threadIdx.x);
   const int m = K / nt;  // separators per thread (host: K = m * nt, m <= MS)
   const int64_t g = blockIdx.x;
@@ -261,22 +248,25 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
   const int j0 = t * m, js = j0 + m - 1;
   if (t == 0) sfail[0] = INT_MAX;
   stime[t] = chunk_begin(js + 1, T, K) - 1;
-  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B>::N) * K;
+  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B, NR>::N) * K;
   int cf = INT_MAX;
   for (int j = j0; j <= js; ++j) cf = min(cf, L.cfail[g * K + j]);
   // ---- eliminate the owned interior separators j0 .. js-1 (spike towards t-1)
   S Lr[MS - 1][B][B];
-  S Lc[B][B], wv[B], X[B][B], All[B][B], rl[B], Pl[B][B];
-  zero<B, S>(Lc); zero<B, S>(wv); zero<B, S>(X); zero<B, S>(All); zero<B, S>(rl);
+  S Lc[B][B], wv[NR][B], X[B][B], All[B][B], rl[NR][B], Pl[B][B];
+  zero<B, S>(Lc); zero<B, S>(X); zero<B, S>(All);
+#pragma unroll
+  for (int p = 0; p < NR; ++p) { zero<B, S>(wv[p]); zero<B, S>(rl[p]); }
   S sg = splat<S>(1.0);
 #pragma unroll
   for (int i = 0; i < MS - 1; ++i) {
-    S D[B][B], r[B], Bl[B][B];
-    psep_ld<B, S>(in, K, L.NT, j0 + min(i, m - 2), D, r, Bl);  // unconditional: lets the loads run ahead
+    S D[B][B], r[NR][B], Bl[B][B];
+    psep_ld<B, S, NR>(in, K, L.NT, j0 + min(i, m - 2), D, r, Bl);  // unconditional: lets the loads run ahead
     if (i < m - 1) {
       if (i == 0) {  // Bl couples to super-separator t - 1 (zero for t = 0)
         lchol<B, S>(D, Lc);
-        llsolve<B, S>(Lc, r, wv);
+#pragma unroll
+        for (int p = 0; p < NR; ++p) llsolve<B, S>(Lc, r[p], wv[p]);
         lleft<B, S>(Lc, Bl, X);
 #pragma unroll
         for (int a = 0; a < B; ++a) {
@@ -287,18 +277,24 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
             for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
             All[a][q] = acc;
           }
-          S acc = mul_(X[0][a], wv[0]);
 #pragma unroll
-          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
-          rl[a] = acc;
+          for (int p = 0; p < NR; ++p) {
+            S acc = mul_(X[0][a], wv[p][0]);
+#pragma unroll
+            for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[p][mm], acc);
+            rl[p][a] = acc;
+          }
         }
       } else {
         S Pm[B][B];  // P = Bl_j L_{j-1}^{-T}
 #pragma unroll
         for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pm[a]);
-        lcouple<B, S>(Pm, wv, D, r);
+        lcouple<B, S>(Pm, wv[0], D, r[0]);
+#pragma unroll
+        for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pm, wv[p], r[p]);
         lchol<B, S>(D, Lc);
-        llsolve<B, S>(Lc, r, wv);
+#pragma unroll
+        for (int p = 0; p < NR; ++p) llsolve<B, S>(Lc, r[p], wv[p]);
         S Y[B][B];
 #pragma unroll
         for (int a = 0; a < B; ++a)
@@ -320,24 +316,29 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
             for (int mm = 0; mm < B; ++mm) acc = fma_(X[mm][a], X[mm][q], acc);
             All[a][q] = acc;
           }
-          S acc = mul_(X[0][a], wv[0]);
 #pragma unroll
-          for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[mm], acc);
-          rl[a] = fma_(sg, acc, rl[a]);
+          for (int p = 0; p < NR; ++p) {
+            S acc = mul_(X[0][a], wv[p][0]);
+#pragma unroll
+            for (int mm = 1; mm < B; ++mm) acc = fma_(X[mm][a], wv[p][mm], acc);
+            rl[p][a] = fma_(sg, acc, rl[p][a]);
+          }
         }
       }
       rcopyL<B, S>(Lc, Lr[i]);
     }
   }
   // ---- the super-separator js: own block minus the interior's Schur terms
-  S Ds[B][B], Rs[B], Bs[B][B];
+  S Ds[B][B], Rs[NR][B], Bs[B][B];
   {
     S Bl[B][B];
-    psep_ld<B, S>(in, K, L.NT, js, Ds, Rs, Bl);
+    psep_ld<B, S, NR>(in, K, L.NT, js, Ds, Rs, Bl);
     if (m > 1) {
 #pragma unroll
       for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pl[a]);
-      lcouple<B, S>(Pl, wv, Ds, Rs);
+      lcouple<B, S>(Pl, wv[0], Ds, Rs[0]);
+#pragma unroll
+      for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pl, wv[p], Rs[p]);
 #pragma unroll
       for (int a = 0; a < B; ++a)
 #pragma unroll
@@ -359,24 +360,31 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
   S* pk = rec + t * BR::N;
 #pragma unroll
   for (int a = 0; a < B; ++a) {
-    rl[a] = neg_(rl[a]);
+#pragma unroll
+    for (int p = 0; p < NR; ++p) rl[p][a] = neg_(rl[p][a]);
 #pragma unroll
     for (int q = 0; q <= a; ++q) All[a][q] = neg_(All[a][q]);
   }
   rst_tri<B, S>(pk + BR::HA, All);
   rst_full<B, S>(pk + BR::HB, Bs);
-  rst_v<B, S>(pk + BR::HR, rl);
+#pragma unroll
+  for (int p = 0; p < NR; ++p) rst_v<B, S>(pk + BR::HR + p * B, rl[p]);
   __syncthreads();
   S Cs[B][B];
   if (t + 1 < nt) {
-    S Al[B][B], An[B][B], rr[B];
+    S Al[B][B], An[B][B];
     const S* pn = rec + (t + 1) * BR::N;
     rld_tri<B, S>(pn + BR::HA, Al);
     rld_full<B, S>(pn + BR::HB, An);
-    rld_v<B, S>(pn + BR::HR, rr);
+#pragma unroll
+    for (int p = 0; p < NR; ++p) {
+      S rr[B];
+      rld_v<B, S>(pn + BR::HR + p * B, rr);
+#pragma unroll
+      for (int a = 0; a < B; ++a) Rs[p][a] = add_(Rs[p][a], rr[a]);
+    }
 #pragma unroll
     for (int a = 0; a < B; ++a) {
-      Rs[a] = add_(Rs[a], rr[a]);
 #pragma unroll
       for (int q = 0; q <= a; ++q) Ds[a][q] = add_(Ds[a][q], Al[a][q]);
 #pragma unroll
@@ -387,61 +395,74 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
   }
   if (cf != INT_MAX) atomicMin(sfail, cf);
   __syncthreads();  // hand-over slots are reused by the reduction
-  rbcr2<B, S>(rec, nt, t, stime, sfail, Ds, Bs, Cs, Rs);
-  S yR[B], yL[B];
-  rld_v<B, S>(rec + t * BR::N + BR::Y, yR);
-  if (t > 0) rld_v<B, S>(rec + (t - 1) * BR::N + BR::Y, yL); else zero<B, S>(yL);
-  // ---- recover the owned separators: forward substitution with y_L, back substitution from y_R
-  S* yo = reinterpret_cast<S*>(L.ysep) + g * int64_t(B) * K;
+  rbcr2n<B, S, NR>(rec, nt, t, stime, sfail, Ds, Bs, Cs, Rs);
+  S yR[NR][B], yL[NR][B];
 #pragma unroll
-  for (int a = 0; a < B; ++a) yo[int64_t(a) * K + js] = yR[a];
-  S Wp[MS - 1][B];
+  for (int p = 0; p < NR; ++p) {
+    rld_v<B, S>(rec + t * BR::N + BR::Y + p * B, yR[p]);
+    if (t > 0) rld_v<B, S>(rec + (t - 1) * BR::N + BR::Y + p * B, yL[p]); else zero<B, S>(yL[p]);
+  }
+  // ---- recover the owned separators: forward substitution with y_L, back substitution from y_R
+  S* yo = reinterpret_cast<S*>(L.ysep) + g * int64_t(NR * B) * K;
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int a = 0; a < B; ++a) yo[int64_t(p * B + a) * K + js] = yR[p][a];
+  S Wp[MS - 1][NR][B];
 #pragma unroll
   for (int i = 0; i < MS - 1; ++i) {
-    S r[B], Bl[B][B];
-    psep_ld_rb<B, S>(in, K, L.NT, j0 + min(i, m - 2), r, Bl);
+    S r[NR][B], Bl[B][B];
+    psep_ld_rb<B, S, NR>(in, K, L.NT, j0 + min(i, m - 2), r, Bl);
     if (i < m - 1) {
-      S tv[B], u[B];
-      if (i == 0) {
 #pragma unroll
-        for (int a = 0; a < B; ++a) tv[a] = yL[a];
-      } else {
-        lltsolve<B, S>(Lr[i - 1], Wp[i - 1], tv);
+      for (int p = 0; p < NR; ++p) {
+        S tv[B], u[B];
+        if (i == 0) {
+#pragma unroll
+          for (int a = 0; a < B; ++a) tv[a] = yL[p][a];
+        } else {
+          lltsolve<B, S>(Lr[i - 1], Wp[i - 1][p], tv);
+        }
+#pragma unroll
+        for (int a = 0; a < B; ++a) {
+          S acc = r[p][a];
+#pragma unroll
+          for (int q = 0; q < B; ++q) acc = fnma_(Bl[a][q], tv[q], acc);
+          u[a] = acc;
+        }
+        llsolve<B, S>(Lr[i], u, Wp[i][p]);
       }
-#pragma unroll
-      for (int a = 0; a < B; ++a) {
-        S acc = r[a];
-#pragma unroll
-        for (int q = 0; q < B; ++q) acc = fnma_(Bl[a][q], tv[q], acc);
-        u[a] = acc;
-      }
-      llsolve<B, S>(Lr[i], u, Wp[i]);
     }
   }
-  S yn[B];
+  S yn[NR][B];
 #pragma unroll
-  for (int a = 0; a < B; ++a) yn[a] = yR[a];
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int a = 0; a < B; ++a) yn[p][a] = yR[p][a];
 #pragma unroll
   for (int i = MS - 2; i >= 0; --i) {
     S Bn[B][B];
-    psep_ld_b<B, S>(in, K, j0 + min(i, m - 2) + 1, Bn);  // coupling (j+1, j)
+    psep_ld_b<B, S, NR>(in, K, j0 + min(i, m - 2) + 1, Bn);  // coupling (j+1, j)
     if (i < m - 1) {
-      S v[B], u[B], tv[B], yv[B];
 #pragma unroll
-      for (int a = 0; a < B; ++a) {
-        S acc = mul_(Bn[0][a], yn[0]);
+      for (int p = 0; p < NR; ++p) {
+        S v[B], u[B], tv[B], yv[B];
 #pragma unroll
-        for (int q = 1; q < B; ++q) acc = fma_(Bn[q][a], yn[q], acc);
-        v[a] = acc;
+        for (int a = 0; a < B; ++a) {
+          S acc = mul_(Bn[0][a], yn[p][0]);
+#pragma unroll
+          for (int q = 1; q < B; ++q) acc = fma_(Bn[q][a], yn[p][q], acc);
+          v[a] = acc;
+        }
+        llsolve<B, S>(Lr[i], v, u);
+#pragma unroll
+        for (int a = 0; a < B; ++a) tv[a] = sub_(Wp[i][p][a], u[a]);
+        lltsolve<B, S>(Lr[i], tv, yv);
+#pragma unroll
+        for (int a = 0; a < B; ++a) yo[int64_t(p * B + a) * K + j0 + i] = yv[a];
+#pragma unroll
+        for (int a = 0; a < B; ++a) yn[p][a] = yv[a];
       }
-      llsolve<B, S>(Lr[i], v, u);
-#pragma unroll
-      for (int a = 0; a < B; ++a) tv[a] = sub_(Wp[i][a], u[a]);
-      lltsolve<B, S>(Lr[i], tv, yv);
-#pragma unroll
-      for (int a = 0; a < B; ++a) yo[int64_t(a) * K + j0 + i] = yv[a];
-#pragma unroll
-      for (int a = 0; a < B; ++a) yn[a] = yv[a];
     }
   }
   if (t == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
@@ -449,7 +470,7 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
 
 
 // ============================================================== P2 ========
-template <int B, class Tio, class S, bool BWD, int CM>
+template <int B, class Tio, class S, bool BWD, int CM, int NR>
 __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? SMNN_PIPE_P2_MINB64 : SMNN_PIPE_P2_MINB64F)
                                                                  : (BWD ? SMNN_PIPE_P2_MINB : SMNN_PIPE_P2_MINB + 1))
     pipe_p2_kernel(Args<Tio> a, PipeL L) {  // forward: 5 CTAs/SM (measured +4 %), backward: 4 (spills at 5)
@@ -461,22 +482,21 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? SMNN_PIP
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.off_bar);
   const Wts<S> w{opaque(splat<S>(a.wg2)), opaque(splat<S>(a.wi2)), opaque(splat<S>(a.ws2))};
   const int64_t tb = g * int64_t(T) * B, t1b = g * int64_t(T), tsb = g * int64_t(T - 1);
-  const int ylo = R.slo;  // BWD: y_fwd from max(ta - 1, 0)
+  const int ylo = R.slo;  // BWD (NR = 1): y_fwd from max(ta - 1, 0)
+  constexpr bool YIN = BWD && NR == 1;  // NR = 2 re-solves y instead of reading it
   const Span<Tio> pc(a.coeffs + tb + R.ta * B, (R.tb - R.ta) * B);
   const Span<Tio> pd(a.rhs + t1b + R.ta, R.tb - R.ta);
   const Span<Tio> ps(a.steps + tsb + R.slo, R.shi - R.slo);
   const Span<Tio> pg(BWD ? a.grad_y + tb + R.ta * B : a.coeffs, BWD ? (R.tb - R.ta) * B : 0);
-  const Span<Tio> py(BWD ? a.y_in + tb + ylo * B : a.coeffs, BWD ? (R.tb - ylo) * B : 0);
+  const Span<Tio> py(YIN ? a.y_in + tb + ylo * B : a.coeffs, YIN ? (R.tb - ylo) * B : 0);
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes);
     bulk_g2s(sm + L.off_c, pc.lo, pc.bytes, bar);
     bulk_g2s(sm + L.off_d, pd.lo, pd.bytes, bar);
     if (ps.bytes) bulk_g2s(sm + L.off_s, ps.lo, ps.bytes, bar);
-    if (BWD) {
-      bulk_g2s(sm + L.off_g, pg.lo, pg.bytes, bar);
-      bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
-    }
+    if (BWD) bulk_g2s(sm + L.off_g, pg.lo, pg.bytes, bar);
+    if (YIN) bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
   }
   constexpr int E = int(sizeof(Tio));
   const int k = R.c0 + tid;
@@ -487,7 +507,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? SMNN_PIP
   // element offsets of the staged streams, relative to global time index 0
   const int oc = L.off_c / E + pc.pre - R.ta * B, od = L.off_d / E + pd.pre - R.ta;
   const int os = L.off_s / E + ps.pre - R.slo;
-  const int og = BWD ? L.off_g / E + pg.pre - R.ta * B : 0, oy = BWD ? L.off_y / E + py.pre - ylo * B : 0;
+  const int og = BWD ? L.off_g / E + pg.pre - R.ta * B : 0, oy = YIN ? L.off_y / E + py.pre - ylo * B : 0;
   Grp<Tio, 1> x;
   x.T = T; x.n_iv = a.n_iv; x.nv = 1;
   x.c.o[0] = oc; x.d.o[0] = od; x.s.o[0] = os; x.gy.o[0] = og; x.yin.o[0] = oy;
@@ -495,7 +515,8 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? SMNN_PIP
   x.u[0] = a.iv + g * a.n_iv;
   x.gu[0] = (BWD && a.g_iv) ? a.g_iv + g * a.n_iv : nullptr;
   x.c.on = x.d.on = x.s.on = true;
-  x.gy.on = x.yin.on = BWD;
+  x.gy.on = BWD;
+  x.yin.on = YIN;
   x.yout.on = !BWD;
   x.gc.on = BWD && a.g_coeffs;
   x.gd.on = BWD && a.g_rhs;
@@ -505,22 +526,25 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? SMNN_PIP
   const Tio* dS = smT + opaque(od + f);
   const Tio* sS = smT + opaque(os + f);
   const Tio* gS = smT + opaque(og + f * B);
-  S yL[B], yR[B];
+  S yL[NR][B], yR[NR][B];
   if (act) {
-    const S* ys = reinterpret_cast<const S*>(L.ysep) + g * int64_t(B) * K + k;
+    const S* ys = reinterpret_cast<const S*>(L.ysep) + g * int64_t(NR * B) * K + k;
 #pragma unroll
-    for (int i = 0; i < B; ++i) yR[i] = ys[int64_t(i) * K];
-    if (k > 0) {
+    for (int p = 0; p < NR; ++p) {
 #pragma unroll
-      for (int i = 0; i < B; ++i) yL[i] = ys[int64_t(i) * K - 1];
-    } else {
-      zero<B, S>(yL);
+      for (int i = 0; i < B; ++i) yR[p][i] = ys[int64_t(p * B + i) * K];
+      if (k > 0) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) yL[p][i] = ys[int64_t(p * B + i) * K - 1];
+      } else {
+        zero<B, S>(yL[p]);
+      }
     }
   }
   __syncthreads();  // barrier initialised
   mbar_wait(bar, 0);
 
-  if (act) p2_chunk<B, Tio, S, BWD, CM>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR);
+  if (act) p2_chunk<B, Tio, S, BWD, CM, NR>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR);
   // ---- outputs: TMA bulk store of the aligned body, plain stores at the ends
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();

@@ -129,16 +129,18 @@ __device__ __forceinline__ void rst_v(S* p, const S (&v)[B]) {
 // Cholesky factorisation of the odd-even permuted separator system (backward
 // stable), unlike PCR.  Record (BRec<B>::N values): L, F, E, g, y, then the
 // pass-1 hand-over (A_ll lower, A_rl, r_l) in slots of its own.
-template <int B>
-struct BRec {
+template <int B, int NR = 1>
+struct BRecN {  // NR right-hand sides share the reduction of the blocks
   static constexpr int LT = B * (B + 1) / 2;  // packed lower triangle
-  static constexpr int L = 0, F = LT, E = LT + B * B, G = LT + 2 * B * B, Y = LT + 2 * B * B + B;
+  static constexpr int L = 0, F = LT, E = LT + B * B, G = LT + 2 * B * B, Y = LT + 2 * B * B + NR * B;
   // pass-1 hand-over (A_ll packed lower, A_rl, r_l) shares the F / E / g slots:
   // read before the first reduction level publishes (one extra barrier)
   static constexpr int HA = F, HB = F + LT, HR = F + LT + B * B;
-  static constexpr int N = (LT + 2 * B * B + 2 * B) | 1;
+  static constexpr int N = (LT + 2 * B * B + 2 * NR * B) | 1;
   static constexpr bool shared_handover = true;
 };
+template <int B>
+using BRec = BRecN<B, 1>;
 
 template <int B, class S>
 __device__ __forceinline__ void rld_tri(const S* p, S (&m)[B][B]) {
@@ -155,10 +157,10 @@ __device__ __forceinline__ void rst_tri(S* p, const S (&m)[B][B]) {
     for (int c = 0; c <= r; ++c) p[r * (r + 1) / 2 + c] = m[r][c];
 }
 
-template <int B, class S>
-__device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, int* sfail, S (&D)[B][B],
-                                      S (&Bl)[B][B], S (&Cr)[B][B], S (&r)[B]) {
-  using Q = BRec<B>;
+template <int B, class S, int NR>
+__device__ __forceinline__ void rbcr2n(S* rec, int K, int k, const int* stime, int* sfail, S (&D)[B][B],
+                                       S (&Bl)[B][B], S (&Cr)[B][B], S (&r)[NR][B]) {
+  using Q = BRecN<B, NR>;
   int bad = 0;
   int hmax = 1;
   while (hmax < K) hmax <<= 1;
@@ -167,25 +169,40 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
   for (int h = 1; h < K; h <<= 1) {
     const int m = k & (2 * h - 1);
     if (m == h) {  // eliminate
-      S Lf[B][B], F[B][B], E[B][B], gv[B];
+      S Lf[B][B], F[B][B], E[B][B];
       bad |= lchol<B, S>(D, Lf);
       lleft<B, S>(Lf, Bl, F);
       lleft<B, S>(Lf, Cr, E);
-      llsolve<B, S>(Lf, r, gv);
       S* pk = rec + k * Q::N;
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        S gv[B];
+        llsolve<B, S>(Lf, r[q], gv);
+        rst_v<B, S>(pk + Q::G + q * B, gv);
+      }
       rst_tri<B, S>(pk + Q::L, Lf);
       rst_full<B, S>(pk + Q::F, F);
       rst_full<B, S>(pk + Q::E, E);
-      rst_v<B, S>(pk + Q::G, gv);
     }
     __syncthreads();
     if (m == 0) {  // survivor: absorb the eliminated neighbours
       if (k - h >= 0) {
         const S* pl = rec + (k - h) * Q::N;
-        S El[B][B], Fl[B][B], gl[B];
+        S El[B][B], Fl[B][B];
         rld_full<B, S>(pl + Q::E, El);
         rld_full<B, S>(pl + Q::F, Fl);
-        rld_v<B, S>(pl + Q::G, gl);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          S gl[B];
+          rld_v<B, S>(pl + Q::G + q * B, gl);
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+            S ar = r[q][i];
+#pragma unroll
+            for (int x = 0; x < B; ++x) ar = fnma_(El[x][i], gl[x], ar);
+            r[q][i] = ar;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < B; ++i) {
 #pragma unroll
@@ -195,10 +212,6 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
             for (int q = 0; q < B; ++q) a = fnma_(El[q][i], El[q][j], a);
             D[i][j] = a;
           }
-          S ar = r[i];
-#pragma unroll
-          for (int q = 0; q < B; ++q) ar = fnma_(El[q][i], gl[q], ar);
-          r[i] = ar;
 #pragma unroll
           for (int j = 0; j < B; ++j) {
             S a = mul_(El[0][i], Fl[0][j]);
@@ -210,10 +223,21 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
       }
       if (k + h < K) {
         const S* pr = rec + (k + h) * Q::N;
-        S Fr[B][B], Er[B][B], gr[B];
+        S Fr[B][B], Er[B][B];
         rld_full<B, S>(pr + Q::F, Fr);
         rld_full<B, S>(pr + Q::E, Er);
-        rld_v<B, S>(pr + Q::G, gr);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          S gr[B];
+          rld_v<B, S>(pr + Q::G + q * B, gr);
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+            S ar = r[q][i];
+#pragma unroll
+            for (int x = 0; x < B; ++x) ar = fnma_(Fr[x][i], gr[x], ar);
+            r[q][i] = ar;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < B; ++i) {
 #pragma unroll
@@ -223,10 +247,6 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
             for (int q = 0; q < B; ++q) a = fnma_(Fr[q][i], Fr[q][j], a);
             D[i][j] = a;
           }
-          S ar = r[i];
-#pragma unroll
-          for (int q = 0; q < B; ++q) ar = fnma_(Fr[q][i], gr[q], ar);
-          r[i] = ar;
 #pragma unroll
           for (int j = 0; j < B; ++j) {
             S a = mul_(Fr[0][i], Er[0][j]);
@@ -241,11 +261,15 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
     }
   }
   if (k == 0) {  // the last survivor
-    S Lf[B][B], t[B], y[B];
+    S Lf[B][B];
     bad |= lchol<B, S>(D, Lf);
-    llsolve<B, S>(Lf, r, t);
-    lltsolve<B, S>(Lf, t, y);
-    rst_v<B, S>(rec + Q::Y, y);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      S t[B], y[B];
+      llsolve<B, S>(Lf, r[q], t);
+      lltsolve<B, S>(Lf, t, y);
+      rst_v<B, S>(rec + Q::Y + q * B, y);
+    }
   }
   if (bad) report<1>(sfail, bad, stime[k]);
 #pragma unroll 1
@@ -253,29 +277,41 @@ __device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, in
     __syncthreads();
     if ((k & (2 * h - 1)) == h) {
       const S* pk = rec + k * Q::N;
-      S Lf[B][B], F[B][B], yl[B], t[B], y[B];
+      S Lf[B][B], F[B][B], E[B][B];
       rld_tri<B, S>(pk + Q::L, Lf);
       rld_full<B, S>(pk + Q::F, F);
-      rld_v<B, S>(pk + Q::G, t);
-      rld_v<B, S>(rec + (k - h) * Q::N + Q::Y, yl);
+      const bool right = k + h < K;
+      if (right) rld_full<B, S>(pk + Q::E, E);
 #pragma unroll
-      for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int q = 0; q < B; ++q) t[i] = fnma_(F[i][q], yl[q], t[i]);
-      if (k + h < K) {
-        S E[B][B], yr[B];
-        rld_full<B, S>(pk + Q::E, E);
-        rld_v<B, S>(rec + (k + h) * Q::N + Q::Y, yr);
+      for (int q = 0; q < NR; ++q) {
+        S yl[B], t[B], y[B];
+        rld_v<B, S>(pk + Q::G + q * B, t);
+        rld_v<B, S>(rec + (k - h) * Q::N + Q::Y + q * B, yl);
 #pragma unroll
         for (int i = 0; i < B; ++i)
 #pragma unroll
-          for (int q = 0; q < B; ++q) t[i] = fnma_(E[i][q], yr[q], t[i]);
+          for (int x = 0; x < B; ++x) t[i] = fnma_(F[i][x], yl[x], t[i]);
+        if (right) {
+          S yr[B];
+          rld_v<B, S>(rec + (k + h) * Q::N + Q::Y + q * B, yr);
+#pragma unroll
+          for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int x = 0; x < B; ++x) t[i] = fnma_(E[i][x], yr[x], t[i]);
+        }
+        lltsolve<B, S>(Lf, t, y);
+        rst_v<B, S>(rec + k * Q::N + Q::Y + q * B, y);
       }
-      lltsolve<B, S>(Lf, t, y);
-      rst_v<B, S>(rec + k * Q::N + Q::Y, y);
     }
   }
   __syncthreads();
+}
+
+// One right-hand side (the rf kernel and the forward pipeline).
+template <int B, class S>
+__device__ __forceinline__ void rbcr2(S* rec, int K, int k, const int* stime, int* sfail, S (&D)[B][B],
+                                      S (&Bl)[B][B], S (&Cr)[B][B], S (&r)[B]) {
+  rbcr2n<B, S, 1>(rec, K, k, stime, sfail, D, Bl, Cr, *reinterpret_cast<S(*)[1][B]>(&r));
 }
 
 

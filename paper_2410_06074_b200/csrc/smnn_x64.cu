@@ -94,33 +94,37 @@ int cur_device() {
   return d;
 }
 
-// Per (device, kernel): dynamic shared memory attribute and whether one
-// cluster of the requested shape fits (cudaOccupancyMaxActiveClusters).
+// Dynamic shared-memory attribute: the largest request so far per (device,
+// kernel) (ensure_smem).  Whether one cluster of the requested shape fits
+// (cudaOccupancyMaxActiveClusters) is cached per (device, kernel, shape).
 template <class K>
 bool prepare(K kern, const XPlan& x, std::string& err) {
   static std::mutex mu;
   static std::map<std::tuple<int, const void*, int, int, size_t>, int> cache;
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), x.smem);
+  if (e == cudaSuccess && x.L.NC > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) {
+    err = std::string("x64 kernel setup: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return false;
+  }
   const auto key = std::make_tuple(cur_device(), reinterpret_cast<const void*>(kern), x.L.NC, x.L.NT, x.smem);
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second > 0;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(x.smem));
-  if (e == cudaSuccess && x.L.NC > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   int ncl = 0;
-  if (e == cudaSuccess) {
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = x.L.NC;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(x.L.NC);
-    cfg.blockDim = dim3(x.L.NT);
-    cfg.dynamicSmemBytes = x.smem;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
-  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = x.L.NC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(x.L.NC);
+  cfg.blockDim = dim3(x.L.NT);
+  cfg.dynamicSmemBytes = x.smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
   if (e != cudaSuccess) {
     err = std::string("x64 kernel setup: ") + cudaGetErrorString(e);
     cudaGetLastError();
@@ -133,7 +137,7 @@ bool prepare(K kern, const XPlan& x, std::string& err) {
 template <int B, class Tio, bool BWD>
 int launch(const smnn_problem* p, const Args<Tio>& a, const XPlan& x, cudaStream_t st, std::string& err) {
   auto kern = x64::x64_kernel<B, Tio, BWD, XC<B, BWD>::value>;
-  if (!prepare(kern, x, err)) return err.empty() ? 0 : -2;
+  if (!prepare(kern, x, err)) return err.empty() ? 0 : SMNN_ERR_CUDA;
   x64::XArgs<Tio> xa;
   xa.coeffs = a.coeffs;
   xa.rhs = a.rhs;
@@ -167,7 +171,8 @@ int launch(const smnn_problem* p, const Args<Tio>& a, const XPlan& x, cudaStream
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("x64 kernel launch: ") + cudaGetErrorString(e);
-    return -2;
+    cudaGetLastError();  // a launch-configuration error must not leak into the next call's check
+    return SMNN_ERR_CUDA;
   }
   return 1;
 }

@@ -81,7 +81,8 @@ def test_kernel_path_selection(lib):
 
 def test_launch_count(lib):
     """smnn_launch_count: one launch for rf / x64 / checkpoint, three for the
-    pipeline; an SMNN_F32_C64 backward on a path that reads y from storage runs
+    pipeline (its SMNN_F32_C64 backward re-solves y with a second right-hand
+    side); an SMNN_F32_C64 backward on a path that reads y from storage runs
     as SMNN_F64 on promoted copies (5 widenings, fp64 forward + backward,
     4 narrowings, 1 info merge)."""
     from paper_2410_06074_b200 import _abi
@@ -93,7 +94,7 @@ def test_launch_count(lib):
     assert count(1000, _abi.SMNN_F32, 0) == 1 and count(1000, _abi.SMNN_F32, 1) == 1
     assert count(10000, _abi.SMNN_F32, 0) == 3
     assert count(10000, _abi.SMNN_F32_C64, 1) == 1                       # x64 re-solves y itself
-    assert count(1000, _abi.SMNN_F32_C64, 1, path=_abi.SMNN_PATH_PIPE) == 5 + 3 + 3 + 4 + 1
+    assert count(1000, _abi.SMNN_F32_C64, 1, path=_abi.SMNN_PATH_PIPE) == 3     # re-solves y (2 rhs)
     assert count(100000, _abi.SMNN_F32_C64, 1) == 5 + 1 + 1 + 4 + 1      # checkpoint kernels, promoted
 
 
