@@ -620,9 +620,10 @@ int launch_fused(const smnn_problem* p, smnn::Args<Tio> a, cudaStream_t st) {
 
 // Kernel path of the fused calls (SMNN_PATH_*; p->path forces one, the
 // parity tests force every path).  Automatic order, measured on B200
-// (profiles/): fp64 arithmetic (SMNN_F64, SMNN_F32_C64) takes the x64
-// cluster-resident kernel while one cluster of <= 16 CTAs holds the instance,
-// then the pipeline, then rf; fp32 arithmetic takes the resident rf kernel
+// (profiles/r2/path_sweep_*.jsonl): fp64 arithmetic (SMNN_F64, SMNN_F32_C64)
+// takes the pipeline (T = 500 .. 2e4 at 4e7 instance-steps: forward equal to or
+// up to 1.8x faster than the x64 cluster kernel, backward 1.2-2.1x faster),
+// then x64, then rf; fp32 arithmetic takes the resident rf kernel
 // while one CTA holds the instance (T <~ 4k: Lorenz 9.3e9 -> 14.4e9
 // instance-steps/s over the checkpoint kernel), then the pipeline (T = 1e4:
 // 7.1e9 -> 22e9); the checkpointing kernels take what none of them fits.
@@ -633,9 +634,9 @@ int kernel_path(const smnn_problem* p, bool bwd) {
   if (want == SMNN_PATH_RF && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
   if (want == SMNN_PATH_PIPE && smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
   if (want == SMNN_PATH_CHECKPOINT || want == SMNN_PATH_STREAM) return SMNN_PATH_CHECKPOINT;
-  if (!f32 && smnn::x64_eligible(p, bwd)) return SMNN_PATH_X64;
   if (f32 && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
   if (smnn::pipe_eligible(p, bwd)) return SMNN_PATH_PIPE;
+  if (!f32 && smnn::x64_eligible(p, bwd)) return SMNN_PATH_X64;
   if (!f32 && smnn::rf_eligible(p, bwd)) return SMNN_PATH_RF;
   return SMNN_PATH_CHECKPOINT;
 }

@@ -61,6 +61,17 @@ WORKLOADS = {
                     desc="configs[3]: SST long-horizon, order-2, D=4096 cells, T=1461 days, fp32"),
     "target": Workload("target", order=2, B=64, D=64, T=10000, s0=0.2, n_iv=2,
                        desc="north_star target: fused fwd+bwd, T=1e4, B*D=4096, order-2, fp32"),
+    # configs[4] scaling-sweep corners (order 2/3, T = 1e2..1e6, B*D up to 65536)
+    "sweep_t1e2": Workload("sweep_t1e2", order=2, B=64, D=1024, T=100, s0=0.2, n_iv=2,
+                           desc="configs[4] corner: T=1e2, B*D=65536, order-2"),
+    "sweep_wide": Workload("sweep_wide", order=2, B=64, D=1024, T=1000, s0=0.2, n_iv=2,
+                           desc="configs[4] corner: T=1e3, B*D=65536, order-2"),
+    "sweep_t1e5": Workload("sweep_t1e5", order=2, B=1, D=64, T=100000, s0=0.2, n_iv=2,
+                           desc="configs[4] corner: T=1e5, B*D=64, order-2"),
+    "sweep_t1e6": Workload("sweep_t1e6", order=2, B=1, D=64, T=1000000, s0=0.2, n_iv=2,
+                           desc="configs[4] corner: T=1e6, B*D=64, order-2"),
+    "sweep_o3_t1e5": Workload("sweep_o3_t1e5", order=3, B=1, D=64, T=100000, s0=0.2, n_iv=3,
+                              desc="configs[4] corner: order-3, T=1e5, B*D=64"),
 }
 
 

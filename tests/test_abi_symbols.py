@@ -68,10 +68,11 @@ def test_kernel_path_selection(lib):
     assert kernel_path(4096, 1461, 2, 2) == "rf"                      # SST (configs[3])
     assert kernel_path(4096, 10000, 2, 2) == "pipe"                   # north_star target, fp32
     assert kernel_path(4096, 10000, 2, 2, bwd=True) == "pipe"
-    assert kernel_path(8192, 2000, 3, 3, compute="f64") == "x64"      # KdV (configs[2])
-    assert kernel_path(4096, 10000, 2, 2, compute="f64") == "x64"     # north_star target, f32c64
-    assert kernel_path(4096, 10000, 2, 2, compute="f64", bwd=True) == "x64"
-    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "x64"
+    assert kernel_path(8192, 2000, 3, 3, compute="f64") == "pipe"     # KdV (configs[2])
+    assert kernel_path(4096, 10000, 2, 2, compute="f64") == "pipe"    # north_star target, f32c64
+    assert kernel_path(4096, 10000, 2, 2, compute="f64", bwd=True) == "pipe"
+    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "pipe"
+    assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64, path="x64") == "x64"
     assert kernel_path(64, 100000, 2, 2, dtype=torch.float64) == "checkpoint"  # > 2048 separators
     assert kernel_path(2, 3, 2, 2) == "checkpoint"                    # too short to chunk
     assert kernel_path(1536, 1000, 2, 2, compute="f64", path="pipe") == "pipe"
@@ -93,7 +94,8 @@ def test_launch_count(lib):
         return lib.smnn_launch_count(ctypes.byref(p), bwd)
     assert count(1000, _abi.SMNN_F32, 0) == 1 and count(1000, _abi.SMNN_F32, 1) == 1
     assert count(10000, _abi.SMNN_F32, 0) == 3
-    assert count(10000, _abi.SMNN_F32_C64, 1) == 1                       # x64 re-solves y itself
+    assert count(10000, _abi.SMNN_F32_C64, 1) == 3                       # pipeline, re-solves y itself
+    assert count(1000, _abi.SMNN_F32_C64, 1, path=_abi.SMNN_PATH_X64) == 1  # x64 re-solves y itself
     assert count(1000, _abi.SMNN_F32_C64, 1, path=_abi.SMNN_PATH_PIPE) == 3     # re-solves y (2 rhs)
     assert count(100000, _abi.SMNN_F32_C64, 1) == 5 + 1 + 1 + 4 + 1      # checkpoint kernels, promoted
 
