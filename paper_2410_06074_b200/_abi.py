@@ -47,11 +47,14 @@ PP = ctypes.POINTER(smnn_problem)
 I32P = ctypes.c_void_p
 
 
-def load(build_if_missing: bool = False) -> ctypes.CDLL:
-    """Load lib/libsmnn.so (RuntimeError if it is not built)."""
+def load(build_if_missing: bool = False, path: str | None = None) -> ctypes.CDLL:
+    """Load lib/libsmnn.so (RuntimeError if it is not built).  `path`: another build of
+    the same library (measurement tools compare compile-time variants; first call only)."""
     global _lib
     if _lib is not None:
         return _lib
+    if path is not None:
+        _build.LIB = path
     if not os.path.exists(_build.LIB):
         if build_if_missing:
             _build.build_library()

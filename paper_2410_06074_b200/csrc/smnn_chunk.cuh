@@ -9,6 +9,8 @@
 //             forward writes y, backward the Appendix A.1 gradient chain.
 #pragma once
 
+#include <type_traits>
+
 #include "smnn_fused.cuh"
 
 namespace smnn {
@@ -115,88 +117,93 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
 #pragma unroll
   for (int q = 0; q < NR; ++q) { zero<B, S>(wv[q]); zero<B, S>(rl[q]); }
   S sg = splat<S>(1.0);
+  // The chunk loop stays rolled (nothing is kept per step): the unrolled body
+  // of fp64 chunks overflowed the instruction cache (ncu: 43 % of the warp
+  // stalls "no instruction" in P1).  Step 0 (no coupling to a previous
+  // interior point) is peeled.
+  auto step = [&](int i, auto first) {
+    constexpr bool FIRST = decltype(first)::value;
+    S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[NR][B];
 #pragma unroll
-  for (int i = 0; i < CM - 1; ++i) {
-    if (i < nint) {
-      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[NR][B];
+    for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
+    spow<B, S>(S(sS[i]), w.s2, an);
+    lassemble<B, S>(c, w.g2, ap, an, M, wc);
+    const bool t0 = FIRST && k == 0;
+    chunk_rhs<B, Tio, S, BWD, NR>(w, n_iv, u, t0, wc, dS, gS, i, rhs);
+    if (t0) {  // initial-value rows at t = 0
 #pragma unroll
-      for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
-      spow<B, S>(S(sS[i]), w.s2, an);
-      lassemble<B, S>(c, w.g2, ap, an, M, wc);
-      const bool t0 = i == 0 && k == 0;
-      chunk_rhs<B, Tio, S, BWD, NR>(w, n_iv, u, t0, wc, dS, gS, i, rhs);
-      if (t0) {  // initial-value rows at t = 0
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-          if (r < n_iv) M[r][r] = add_(M[r][r], w.i2);
-      }
-      if (i == 0) {
-        lchol<B, S>(M, Lc);
-#pragma unroll
-        for (int q = 0; q < NR; ++q) llsolve<B, S>(Lc, rhs[q], wv[q]);
-        S NL[B][B];  // spike X_f = L_f^{-1} N_{f-1} (zero for k = 0: ap = 0)
-        lN<B, S>(ap, NL);
-        lleft<B, S>(Lc, NL, X);
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-#pragma unroll
-          for (int q = 0; q <= r; ++q) {
-            S acc = mul_(X[0][r], X[0][q]);
-#pragma unroll
-            for (int m = 1; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
-            All[r][q] = acc;
-          }
-#pragma unroll
-          for (int q = 0; q < NR; ++q) {
-            S acc = mul_(X[0][r], wv[q][0]);
-#pragma unroll
-            for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[q][m], acc);
-            rl[q][r] = acc;
-          }
-        }
-      } else {
-        S Pm[B][B];
-        lPfromN<B, S>(ap, Lc, Pm);  // P_{j-1} = N_{j-1} L_{j-1}^{-T}
-        lcouple<B, S>(Pm, wv[0], M, rhs[0]);
-#pragma unroll
-        for (int q = 1; q < NR; ++q) lcouple_v<B, S>(Pm, wv[q], rhs[q]);
-        lchol<B, S>(M, Lc);
-#pragma unroll
-        for (int q = 0; q < NR; ++q) llsolve<B, S>(Lc, rhs[q], wv[q]);
-        S Y[B][B];  // spike X_j = -L_j^{-1} P_{j-1} X_{j-1}, carried with sign sg
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-#pragma unroll
-          for (int q = 0; q < B; ++q) {
-            S acc = mul_(Pm[r][0], X[0][q]);
-#pragma unroll
-            for (int m = 1; m < B; ++m) acc = fma_(Pm[r][m], X[m][q], acc);
-            Y[r][q] = acc;
-          }
-        lleft<B, S>(Lc, Y, X);
-        sg = neg_(sg);
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-#pragma unroll
-          for (int q = 0; q <= r; ++q) {
-            S acc = All[r][q];
-#pragma unroll
-            for (int m = 0; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
-            All[r][q] = acc;
-          }
-#pragma unroll
-          for (int q = 0; q < NR; ++q) {
-            S acc = mul_(X[0][r], wv[q][0]);
-#pragma unroll
-            for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[q][m], acc);
-            rl[q][r] = fma_(sg, acc, rl[q][r]);
-          }
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+      for (int r = 0; r < B; ++r)
+        if (r < n_iv) M[r][r] = add_(M[r][r], w.i2);
     }
-  }
+    if constexpr (FIRST) {
+      lchol<B, S>(M, Lc);
+#pragma unroll
+      for (int q = 0; q < NR; ++q) llsolve<B, S>(Lc, rhs[q], wv[q]);
+      S NL[B][B];  // spike X_f = L_f^{-1} N_{f-1} (zero for k = 0: ap = 0)
+      lN<B, S>(ap, NL);
+      lleft<B, S>(Lc, NL, X);
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+#pragma unroll
+        for (int q = 0; q <= r; ++q) {
+          S acc = mul_(X[0][r], X[0][q]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
+          All[r][q] = acc;
+        }
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          S acc = mul_(X[0][r], wv[q][0]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[q][m], acc);
+          rl[q][r] = acc;
+        }
+      }
+    } else {
+      S Pm[B][B];
+      lPfromN<B, S>(ap, Lc, Pm);  // P_{j-1} = N_{j-1} L_{j-1}^{-T}
+      lcouple<B, S>(Pm, wv[0], M, rhs[0]);
+#pragma unroll
+      for (int q = 1; q < NR; ++q) lcouple_v<B, S>(Pm, wv[q], rhs[q]);
+      lchol<B, S>(M, Lc);
+#pragma unroll
+      for (int q = 0; q < NR; ++q) llsolve<B, S>(Lc, rhs[q], wv[q]);
+      S Y[B][B];  // spike X_j = -L_j^{-1} P_{j-1} X_{j-1}, carried with sign sg
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          S acc = mul_(Pm[r][0], X[0][q]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) acc = fma_(Pm[r][m], X[m][q], acc);
+          Y[r][q] = acc;
+        }
+      lleft<B, S>(Lc, Y, X);
+      sg = neg_(sg);
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+#pragma unroll
+        for (int q = 0; q <= r; ++q) {
+          S acc = All[r][q];
+#pragma unroll
+          for (int m = 0; m < B; ++m) acc = fma_(X[m][r], X[m][q], acc);
+          All[r][q] = acc;
+        }
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          S acc = mul_(X[0][r], wv[q][0]);
+#pragma unroll
+          for (int m = 1; m < B; ++m) acc = fma_(X[m][r], wv[q][m], acc);
+          rl[q][r] = fma_(sg, acc, rl[q][r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+  };
+  step(0, std::true_type{});
+#pragma unroll 1
+  for (int i = 1; i < nint; ++i) step(i, std::false_type{});
   // one pivot check per chunk: a breakdown leaves a non-finite last factor
   const bool bad = bad_(splat<S>(1.0) / Lc[B - 1][B - 1]) != 0;
   {  // Schur complement of the interior onto (sigma_{k-1}, sigma_k); ap = a(s_l)
@@ -241,55 +248,63 @@ __device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, in
   S Wp[(STORE && !WSM) ? HM : 1][NR][B];
   S ap[2 * B - 1];
   if (i0 > 0 || k > 0) spow<B, S>(S(sS[i0 - 1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
+  // forward sweep step q (point i = i0 + q); STORE keeps factor and w' per
+  // step in registers (fully unrolled), the run-through keeps only the last
+  // (rolled loop: small code, see p1_chunk)
+  auto fstep = [&](int q) {
+    const int i = i0 + q;
+    S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[NR][B];
 #pragma unroll
-  for (int q = 0; q < HM; ++q) {
-    if (q < len) {
-      const int i = i0 + q;
-      S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[NR][B];
+    for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
+    spow<B, S>(S(sS[i]), w.s2, an);
+    lassemble<B, S>(c, w.g2, ap, an, M, wc);
+    const bool t0 = i == 0 && k == 0;
+    chunk_rhs<B, Tio, S, BWD, NR>(w, x.n_iv, x.u[0], t0, wc, dS, gS, i, rhs);
+    if (i == 0) {  // chunk start (q == 0, i0 == 0)
+      if (t0) {
 #pragma unroll
-      for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
-      spow<B, S>(S(sS[i]), w.s2, an);
-      lassemble<B, S>(c, w.g2, ap, an, M, wc);
-      const bool t0 = i == 0 && k == 0;
-      chunk_rhs<B, Tio, S, BWD, NR>(w, x.n_iv, x.u[0], t0, wc, dS, gS, i, rhs);
-      if (i == 0) {  // chunk start (q == 0, i0 == 0)
-        if (t0) {
-#pragma unroll
-          for (int r = 0; r < B; ++r)
-            if (r < x.n_iv) M[r][r] = add_(M[r][r], w.i2);
-        }
-#pragma unroll
-        for (int p = 0; p < NR; ++p) {  // rhs -= N_{f-1} y_L
-          S Nt[B];
-          rNv<B, S>(ap, yL[p], Nt);
-#pragma unroll
-          for (int r = 0; r < B; ++r) rhs[p][r] = sub_(rhs[p][r], Nt[r]);
-        }
-      } else {
-        S Pm[B][B];
-        lPfromN<B, S>(ap, (STORE && q > 0) ? Lr[STORE ? (q > 0 ? q - 1 : 0) : 0] : Ls, Pm);
-        lcouple<B, S>(Pm, ws[0], M, rhs[0]);
-#pragma unroll
-        for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pm, ws[p], rhs[p]);
-      }
-      S Lc[B][B];
-      lchol<B, S>(M, Lc);
-#pragma unroll
-      for (int p = 0; p < NR; ++p) llsolve<B, S>(Lc, rhs[p], ws[p]);
-      if (STORE) {
-        rcopyL<B, S>(Lc, Lr[STORE ? q : 0]);
-#pragma unroll
-        for (int p = 0; p < NR; ++p)
-#pragma unroll
-          for (int r = 0; r < B; ++r) {
-            if (WSM) wS[i * B + r] = Tio(ws[p][r]); else Wp[(STORE && !WSM) ? q : 0][p][r] = ws[p][r];
-          }
-      } else {
-        rcopyL<B, S>(Lc, Ls);
+        for (int r = 0; r < B; ++r)
+          if (r < x.n_iv) M[r][r] = add_(M[r][r], w.i2);
       }
 #pragma unroll
-      for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+      for (int p = 0; p < NR; ++p) {  // rhs -= N_{f-1} y_L
+        S Nt[B];
+        rNv<B, S>(ap, yL[p], Nt);
+#pragma unroll
+        for (int r = 0; r < B; ++r) rhs[p][r] = sub_(rhs[p][r], Nt[r]);
+      }
+    } else {
+      S Pm[B][B];
+      lPfromN<B, S>(ap, (STORE && q > 0) ? Lr[STORE ? (q > 0 ? q - 1 : 0) : 0] : Ls, Pm);
+      lcouple<B, S>(Pm, ws[0], M, rhs[0]);
+#pragma unroll
+      for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pm, ws[p], rhs[p]);
     }
+    S Lc[B][B];
+    lchol<B, S>(M, Lc);
+#pragma unroll
+    for (int p = 0; p < NR; ++p) llsolve<B, S>(Lc, rhs[p], ws[p]);
+    if (STORE) {
+      rcopyL<B, S>(Lc, Lr[STORE ? q : 0]);
+#pragma unroll
+      for (int p = 0; p < NR; ++p)
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          if (WSM) wS[i * B + r] = Tio(ws[p][r]); else Wp[(STORE && !WSM) ? q : 0][p][r] = ws[p][r];
+        }
+    } else {
+      rcopyL<B, S>(Lc, Ls);
+    }
+#pragma unroll
+    for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
+  };
+  if constexpr (STORE) {
+#pragma unroll
+    for (int q = 0; q < HM; ++q)
+      if (q < len) fstep(q);
+  } else {
+#pragma unroll 1
+    for (int q = 0; q < len; ++q) fstep(q);
   }
   if (!STORE) return;
 #pragma unroll

@@ -54,6 +54,9 @@ namespace smnn {
 #ifndef SMNN_PIPE_P2_MINB64
 #define SMNN_PIPE_P2_MINB64 3
 #endif
+#ifndef SMNN_PIPE_P2_MINB64R  // backward with two right-hand sides (SMNN_F32_C64)
+#define SMNN_PIPE_P2_MINB64R 3
+#endif
 #ifndef SMNN_PIPE_P2_MINB64F
 #define SMNN_PIPE_P2_MINB64F 4
 #endif
@@ -471,7 +474,8 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
 
 // ============================================================== P2 ========
 template <int B, class Tio, class S, bool BWD, int CM, int NR>
-__global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? SMNN_PIPE_P2_MINB64 : SMNN_PIPE_P2_MINB64F)
+__global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? (NR == 2 ? SMNN_PIPE_P2_MINB64R : SMNN_PIPE_P2_MINB64)
+                                                                        : SMNN_PIPE_P2_MINB64F)
                                                                  : (BWD ? SMNN_PIPE_P2_MINB : SMNN_PIPE_P2_MINB + 1))
     pipe_p2_kernel(Args<Tio> a, PipeL L) {  // forward: 5 CTAs/SM (measured +4 %), backward: 4 (spills at 5)
   unsigned char* sm = smnn_dyn_smem;

@@ -25,7 +25,11 @@ ap.add_argument("--order", type=int, default=2)
 ap.add_argument("--units", type=float, default=4e7)
 ap.add_argument("--T", default="500,1000,1461,2000,3000,4000,5000,7500,10000,15000,20000")
 ap.add_argument("--paths", default="auto,x64,pipe,checkpoint")
+ap.add_argument("--lib", default=None, help="a variant build (tools/build_variant.sh)")
 a = ap.parse_args()
+if a.lib:
+    from paper_2410_06074_b200 import _abi
+    _abi.load(path=a.lib)
 tdt = torch.float64 if a.dtype == "f64" else torch.float32
 compute = "f64" if a.dtype == "f32c64" else None
 R = a.order
