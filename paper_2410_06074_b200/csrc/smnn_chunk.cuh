@@ -384,6 +384,8 @@ __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, 
   if (CM - 1 <= HM || nint <= HM) {
     p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, 0, nint, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
   } else {
+    // (measured: calling one stored-segment copy twice from a rolled loop
+    // shrinks the code but costs more instructions than the icache saves)
     const int h = nint - HM;
     p2_seg<B, Tio, S, BWD, HM, false, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
     p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, h, HM, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
