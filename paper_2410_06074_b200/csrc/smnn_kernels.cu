@@ -816,7 +816,7 @@ int smnn_launch_count(const smnn_problem* p, int bwd) {
     const int io = p->T > 1 ? 5 : 4;
     return io + smnn_launch_count(&q, 0) + smnn_launch_count(&q, 1) + (io - 1) + 1;
   }
-  return kernel_path(p, bwd != 0) == SMNN_PATH_PIPE ? 3 : 1;
+  return kernel_path(p, bwd != 0) == SMNN_PATH_PIPE ? smnn::pipe_launches(p, bwd != 0) : 1;
 }
 
 size_t smnn_workspace_bytes(const smnn_problem* p) {

@@ -18,8 +18,16 @@ namespace {
 size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// fp64 separator kernel: 8 separators per thread (K/8 threads per instance,
+// up to 4 instances per SM at the same 128 registers) from this K on
+#ifndef SMNN_PIPE_M8_64
+#define SMNN_PIPE_M8_64 (1 << 30)
+#endif
+
 template <int B>
 size_t nr_sep_fields(int nr) { return nr == 2 ? size_t(PSep<B, 2>::N) : size_t(PSep<B, 1>::N); }
+
+constexpr int kMaxLevels = 3;  // separator hierarchy: up to 2048 * 8^3 level-0 separators
 
 struct PipePlan {
   bool ok = false;
@@ -27,8 +35,14 @@ struct PipePlan {
   bool sep2 = false;  // separator kernel: pipe_sep2_kernel (K/m2 threads, m2 separators each)
   int m2 = 4;
   size_t smem_p1 = 0, smem_p2 = 0, smem_sep = 0;
-  size_t ws_sep1 = 0, ws_ysep = 0, ws_fail = 0;
+  size_t ws_sep1 = 0, ws_ysep = 0, ws_fail = 0;  // level 0
   PipeL L1{}, L2{};
+  // hierarchical separators (K > 2048): levels 1..levels, K_l = K / 8^l, the
+  // top level solved by the separator kernel
+  int levels = 0;
+  int Kl[kMaxLevels + 1] = {};
+  size_t off_rec[kMaxLevels + 1] = {}, off_y[kMaxLevels + 1] = {}, off_fail[kMaxLevels + 1] = {};
+  size_t ws_total = 0;
 };
 
 // Right-hand sides of a pipeline call: 2 in the SMNN_F32_C64 backward (dl/dy and
@@ -49,13 +63,31 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     const int q128 = K > 1024 ? 256 : 128;
     K = std::min((K + q128 - 1) / q128 * q128, T / 2);
   }
-  if (K < 1 || K > SMNN_PIPE_SEP_MAX || (T + K - 1) / K > CM) return q;
-  q.sep2 = K > 256 && K % 128 == 0;
-  if (q.sep2) {  // separators per thread: 4, or 8 when K/4 would exceed 256 threads
-    q.m2 = K / 4 > 256 ? 8 : 4;
-    if (K % (32 * q.m2) != 0 || K / q.m2 > 256) q.sep2 = false;
+  int levels = 0, Ktop = K;
+  if (K > SMNN_PIPE_SEP_MAX) {  // separator hierarchy: 8 separators per thread and level
+    const int64_t kmin = (int64_t(T) + CM - 1) / CM;
+    for (levels = 1; levels <= kMaxLevels; ++levels) {
+      int64_t f = 1;
+      for (int l = 0; l < levels; ++l) f *= kSepLM;
+      const int64_t unit = f * 256;  // top level: a multiple of 256 separators (sep2 divisibility)
+      const int64_t K0 = (kmin + unit - 1) / unit * unit;
+      if (K0 / f <= SMNN_PIPE_SEP_MAX) {
+        K = K0 <= T / 2 && K0 < (int64_t(1) << 30) ? int(K0) : 0;
+        Ktop = int(K0 / f);
+        break;
+      }
+    }
+    if (levels > kMaxLevels || K == 0) return q;
   }
-  if (K > 256 && !q.sep2) return q;
+  if (K < 1 || Ktop > SMNN_PIPE_SEP_MAX || (T + K - 1) / K > CM) return q;
+  q.levels = levels;
+  for (int l = 0, k = K; l <= levels; ++l, k /= kSepLM) q.Kl[l] = k;
+  q.sep2 = Ktop > 256 && Ktop % 128 == 0;
+  if (q.sep2) {  // separators per thread: 4, or 8 when K/4 would exceed 256 threads
+    q.m2 = (Ktop / 4 > 256 || (sizeof(S) >= 8 && Ktop >= SMNN_PIPE_M8_64)) ? 8 : 4;
+    if (Ktop % (32 * q.m2) != 0 || Ktop / q.m2 > 256) q.sep2 = false;
+  }
+  if (Ktop > 256 && !q.sep2) return q;
   const size_t ls = sizeof(S);
   q.K = K;
   q.CM = CM;
@@ -88,13 +120,26 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
   }
   q.parts = (K + q.NT - 1) / q.NT;
   const size_t recn = nr == 2 ? size_t(BRecN<B, 2>::N) : size_t(BRecN<B, 1>::N);
-  q.smem_sep = recn * (q.sep2 ? K / q.m2 : K) * ls + size_t(2 * K + 4) * 4;
+  q.smem_sep = recn * (q.sep2 ? Ktop / q.m2 : Ktop) * ls + size_t(2 * Ktop + 4) * 4;
   if (q.smem_p1 > 200 * 1024 || q.smem_p2 > 200 * 1024 || q.smem_sep > 220 * 1024) return q;
-  q.ws_sep1 = al256(size_t(p->n_inst) * (nr == 2 ? PSep<B, 2>::N : PSep<B, 1>::N) * K * ls);
-  q.ws_ysep = al256(size_t(p->n_inst) * nr * B * K * ls);
-  q.ws_fail = al256(size_t(p->n_inst) * K * 4);
+  const size_t nrec = nr == 2 ? PSep<B, 2>::N : PSep<B, 1>::N;
+  size_t off = 0;
+  for (int l = 0; l <= levels; ++l) {  // per level: records, y at the separators, failure flags
+    q.off_rec[l] = off;
+    off += al256(size_t(p->n_inst) * nrec * q.Kl[l] * ls);
+    q.off_y[l] = off;
+    off += al256(size_t(p->n_inst) * nr * B * q.Kl[l] * ls);
+    q.off_fail[l] = off;
+    off += al256(size_t(p->n_inst) * q.Kl[l] * 4);
+  }
+  q.ws_total = off;
+  q.ws_sep1 = q.off_y[0];
+  q.ws_ysep = q.off_fail[0] - q.off_y[0];
+  q.ws_fail = (levels > 0 ? q.off_rec[1] : off) - q.off_fail[0];
   for (PipeL* L : {&q.L1, &q.L2}) {
     L->K = K;
+    L->K0 = K;
+    L->sstride = 1;
     L->NT = q.NT;
     L->parts = q.parts;
   }
@@ -138,43 +183,41 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   const int64_t n = p->n_inst;
   if (n <= 0) return 1;
   const int T = p->T, K = q.K;
-  const size_t ls = sizeof(S);
-  const size_t rec = nr_sep_fields<B>(NR);
   char* ws = static_cast<char*>(a.ckpt);
-  // one chain (P1 -> SEP -> P2) over instances [i0, i1) on stream s
-  auto chain = [&](int64_t i0, int64_t i1, cudaStream_t s) {
-    const int64_t ni = i1 - i0;
-    Args<Tio> ag = a;
-    ag.n_inst = ni;
-    ag.coeffs = a.coeffs + i0 * T * B;
-    ag.rhs = a.rhs + i0 * T;
-    ag.iv = a.iv + i0 * a.n_iv;
-    ag.steps = a.steps + i0 * (T - 1);
-    if (a.y_in) ag.y_in = a.y_in + i0 * T * B;
-    if (a.grad_y) ag.grad_y = a.grad_y + i0 * T * B;
-    if (a.y_out) ag.y_out = a.y_out + i0 * T * B;
-    if (a.g_coeffs) ag.g_coeffs = a.g_coeffs + i0 * T * B;
-    if (a.g_rhs) ag.g_rhs = a.g_rhs + i0 * T;
-    if (a.g_iv) ag.g_iv = a.g_iv + i0 * a.n_iv;
-    if (a.g_steps) ag.g_steps = a.g_steps + i0 * (T - 1);
-    int32_t* info = a.info ? a.info + i0 : nullptr;
-    PipeL L1 = q.L1, L2 = q.L2;
-    for (PipeL* L : {&L1, &L2}) {  // workspace: separator records, separator solution, chunk failure flags
-      L->sep1 = ws + size_t(i0) * rec * K * ls;
-      L->ysep = ws + q.ws_sep1 + size_t(i0) * NR * B * K * ls;
-      L->cfail = reinterpret_cast<int*>(ws + q.ws_sep1 + q.ws_ysep) + i0 * K;
-    }
-    k1<<<unsigned(ni * q.parts), q.NT, q.smem_p1, s>>>(ag, L1);
+  auto level = [&](int l) {  // PipeL of separator level l (l = 0: the chunk kernels' view)
+    PipeL L = q.L1;
+    L.K = q.Kl[l];
+    L.K0 = K;
+    int st = 1;
+    for (int i = 0; i < l; ++i) st *= kSepLM;
+    L.sstride = st;
+    L.NT = l == 0 ? q.NT : kSepLNT;  // CTA size of the kernel that wrote the level's records
+    L.sep1 = ws + q.off_rec[l];
+    L.ysep = ws + q.off_y[l];
+    L.cfail = reinterpret_cast<int*>(ws + q.off_fail[l]);
+    return L;
+  };
+  auto chain = [&](cudaStream_t s) {
+    PipeL L1 = level(0), L2 = level(0);
+    L2.off_c = q.L2.off_c; L2.off_d = q.L2.off_d; L2.off_s = q.L2.off_s; L2.off_g = q.L2.off_g;
+    L2.off_y = q.L2.off_y; L2.off_h = q.L2.off_h; L2.off_bar = q.L2.off_bar;
+    k1<<<unsigned(n * q.parts), q.NT, q.smem_p1, s>>>(a, L1);
+    for (int l = 0; l < q.levels; ++l)
+      pipe_sepl_kernel<B, S, NR><<<unsigned(n * (q.Kl[l] / (kSepLM * kSepLNT))), kSepLNT, 0, s>>>(level(l), level(l + 1),
+                                                                                                    T);
+    const PipeL Lt = level(q.levels);
     if (q.sep2)
-      k2b<<<unsigned(ni), q.K / q.m2, q.smem_sep, s>>>(L1, T, info);
+      k2b<<<unsigned(n), Lt.K / q.m2, q.smem_sep, s>>>(Lt, T, a.info);
     else
-      k2<<<unsigned(ni), q.K, q.smem_sep, s>>>(L1, T, info);
-    k3<<<unsigned(ni * q.parts), q.NT, q.smem_p2, s>>>(ag, L2);
+      k2<<<unsigned(n), Lt.K, q.smem_sep, s>>>(Lt, T, a.info);
+    for (int l = q.levels - 1; l >= 0; --l)
+      pipe_sepr_kernel<B, S, NR><<<unsigned(n * (q.Kl[l] / (kSepLM * kSepLNT))), kSepLNT, 0, s>>>(level(l), level(l + 1));
+    k3<<<unsigned(n * q.parts), q.NT, q.smem_p2, s>>>(a, L2);
   };
   // (measured: splitting the instances into 2 groups on separate streams, so
   // one group's separator kernel overlaps the other's chunk kernels, gave no
   // gain on the f32c64 target -- 2.80 vs 2.68 ms backward)
-  chain(0, n, st);
+  chain(st);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("pipeline launch: ") + cudaGetErrorString(e);
@@ -206,11 +249,16 @@ int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std
 
 bool pipe_eligible(const smnn_problem* p, bool bwd) { return plan_of(p, bwd).ok; }
 
+int pipe_launches(const smnn_problem* p, bool bwd) {
+  const PipePlan q = plan_of(p, bwd);
+  return q.ok ? 3 + 2 * q.levels : 0;
+}
+
 size_t pipe_workspace_bytes(const smnn_problem* p) {
   const PipePlan f = plan_of(p, false), b = plan_of(p, true);
   size_t n = 0;
-  if (f.ok) n = std::max(n, f.ws_sep1 + f.ws_ysep + f.ws_fail);
-  if (b.ok) n = std::max(n, b.ws_sep1 + b.ws_ysep + b.ws_fail);
+  if (f.ok) n = std::max(n, f.ws_total);
+  if (b.ok) n = std::max(n, b.ws_total);
   return n;
 }
 

@@ -68,7 +68,9 @@ namespace smnn {
 #endif
 
 struct PipeL {
-  int K;          // chunks (= separators) per instance
+  int K;          // chunks (= separators) per instance (at this level of the separator hierarchy)
+  int K0;         // level-0 separators (time mapping for `info`)
+  int sstride;    // level-0 separators per separator of this level (8^level)
   int NT;         // threads per CTA of the chunk kernels
   int parts;      // CTAs per instance of the chunk kernels
   int off_c, off_d, off_s, off_g, off_y, off_h, off_bar;  // shared-memory byte offsets (16-aligned)
@@ -93,6 +95,12 @@ struct PRange {
     shi = min(tb, T - 1);
   }
 };
+
+// Time index of separator j of a level whose separators are every
+// L.sstride-th level-0 separator (error reporting, include/smnn.h `info`).
+__device__ __forceinline__ int sep_time(const PipeL& L, int j, int T) {
+  return chunk_begin(int(int64_t(j + 1) * L.sstride), T, L.K0) - 1;
+}
 
 // ============================================================== P1 ========
 template <int B, class Tio, class S, bool BWD, int CM, int NR>
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
   int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * K);
   int* sfail = stime + K;
   if (k == 0) sfail[0] = INT_MAX;
-  stime[k] = chunk_begin(k + 1, T, K) - 1;
+  stime[k] = sep_time(L, k, T);
   const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B, NR>::N) * K;
   S D[B][B], Bl[B][B], Cr[B][B], r[NR][B];
   psep_ld<B, S, NR>(in, K, L.NT, k, D, r, Bl);  // own block + A_ll, r_l across a P1 CTA boundary
@@ -237,26 +245,20 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
 // the first m - 1 (with the spike towards super-separator t - 1, factors kept
 // in registers), the K/m super-separators j0 + m - 1 are solved by rbcr2, and
 // the owned separators are recovered by forward + back substitution.
+// Local elimination of the m separators j0 .. j0 + m - 1 one thread owns
+// (m <= MS): block Cholesky of the first m - 1 with the spike towards the
+// previous super-separator (factors Lr and forward-substituted rhs wv kept),
+// then the super-separator js = j0 + m - 1: its block minus the interior's
+// Schur terms (Ds, Rs), its coupling to the previous super-separator (Bs) and
+// the hand-over sums (All = sum X^T X, rl = sum X^T w; negated by the caller).
+// Returns true on a pivot breakdown.  Shared by pipe_sep2_kernel (one level)
+// and the hierarchical separator kernels (pipe_sepl_kernel / pipe_sepr_kernel).
 template <int B, class S, int MS, int NR>
-__global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
-  using BR = BRecN<B, NR>;
-  unsigned char* sm = smnn_dyn_smem;
-  const int K = L.K, nt = blockDim.x;
-  const int t = int(threadIdx.x);
-  const int m = K / nt;  // separators per thread (host: K = m * nt, m <= MS)
-  const int64_t g = blockIdx.x;
-  S* rec = reinterpret_cast<S*>(sm);
-  int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * nt);
-  int* sfail = stime + nt;
-  const int j0 = t * m, js = j0 + m - 1;
-  if (t == 0) sfail[0] = INT_MAX;
-  stime[t] = chunk_begin(js + 1, T, K) - 1;
-  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B, NR>::N) * K;
-  int cf = INT_MAX;
-  for (int j = j0; j <= js; ++j) cf = min(cf, L.cfail[g * K + j]);
-  // ---- eliminate the owned interior separators j0 .. js-1 (spike towards t-1)
-  S Lr[MS - 1][B][B];
-  S Lc[B][B], wv[NR][B], X[B][B], All[B][B], rl[NR][B], Pl[B][B];
+__device__ __forceinline__ bool sep_local(const S* in, int K, int NTin, int j0, int m, S (&Lr)[MS - 1][B][B],
+                                          S (&Ds)[B][B], S (&Rs)[NR][B], S (&Bs)[B][B], S (&All)[B][B],
+                                          S (&rl)[NR][B]) {
+  const int js = j0 + m - 1;
+  S Lc[B][B], wv[NR][B], X[B][B], Pl[B][B];
   zero<B, S>(Lc); zero<B, S>(X); zero<B, S>(All);
 #pragma unroll
   for (int p = 0; p < NR; ++p) { zero<B, S>(wv[p]); zero<B, S>(rl[p]); }
@@ -264,9 +266,9 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
 #pragma unroll
   for (int i = 0; i < MS - 1; ++i) {
     S D[B][B], r[NR][B], Bl[B][B];
-    psep_ld<B, S, NR>(in, K, L.NT, j0 + min(i, m - 2), D, r, Bl);  // unconditional: lets the loads run ahead
+    psep_ld<B, S, NR>(in, K, NTin, j0 + min(i, max(m - 2, 0)), D, r, Bl);  // unconditional: loads run ahead
     if (i < m - 1) {
-      if (i == 0) {  // Bl couples to super-separator t - 1 (zero for t = 0)
+      if (i == 0) {  // Bl couples to the previous super-separator (zero for the first)
         lchol<B, S>(D, Lc);
 #pragma unroll
         for (int p = 0; p < NR; ++p) llsolve<B, S>(Lc, r[p], wv[p]);
@@ -332,33 +334,123 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
     }
   }
   // ---- the super-separator js: own block minus the interior's Schur terms
-  S Ds[B][B], Rs[NR][B], Bs[B][B];
-  {
-    S Bl[B][B];
-    psep_ld<B, S, NR>(in, K, L.NT, js, Ds, Rs, Bl);
-    if (m > 1) {
+  S Bl[B][B];
+  psep_ld<B, S, NR>(in, K, NTin, js, Ds, Rs, Bl);
+  if (m > 1) {
 #pragma unroll
-      for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pl[a]);
-      lcouple<B, S>(Pl, wv[0], Ds, Rs[0]);
+    for (int a = 0; a < B; ++a) llsolve<B, S>(Lc, Bl[a], Pl[a]);
+    lcouple<B, S>(Pl, wv[0], Ds, Rs[0]);
 #pragma unroll
-      for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pl, wv[p], Rs[p]);
+    for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pl, wv[p], Rs[p]);
 #pragma unroll
-      for (int a = 0; a < B; ++a)
+    for (int a = 0; a < B; ++a)
 #pragma unroll
-        for (int q = 0; q < B; ++q) {
-          S acc = mul_(Pl[a][0], X[0][q]);
+      for (int q = 0; q < B; ++q) {
+        S acc = mul_(Pl[a][0], X[0][q]);
 #pragma unroll
-          for (int mm = 1; mm < B; ++mm) acc = fma_(Pl[a][mm], X[mm][q], acc);
-          Bs[a][q] = mul_(neg_(sg), acc);
+        for (int mm = 1; mm < B; ++mm) acc = fma_(Pl[a][mm], X[mm][q], acc);
+        Bs[a][q] = mul_(neg_(sg), acc);
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < B; ++a)
+#pragma unroll
+      for (int q = 0; q < B; ++q) Bs[a][q] = Bl[a][q];
+  }
+  return m > 1 && bad_(splat<S>(1.0) / Lc[B - 1][B - 1]) != 0;
+}
+
+// Recovery of the owned separators j0 .. j0 + m - 2 from the factors Lr of
+// sep_local and the solutions at the neighbouring super-separators (yL: the
+// previous one, yR: own, js): forward substitution with yL, back substitution
+// from yR.  Writes y of all m owned separators to yo ([NR B][Kout] field-major).
+template <int B, class S, int MS, int NR>
+__device__ __forceinline__ void sep_recover(const S* in, int K, int NTin, int j0, int m,
+                                            const S (&Lr)[MS - 1][B][B], const S (&yL)[NR][B],
+                                            const S (&yR)[NR][B], S* yo, int64_t Kout) {
+  const int js = j0 + m - 1;
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int a = 0; a < B; ++a) yo[int64_t(p * B + a) * Kout + js] = yR[p][a];
+  S Wp[MS - 1][NR][B];
+#pragma unroll
+  for (int i = 0; i < MS - 1; ++i) {
+    S r[NR][B], Bl[B][B];
+    psep_ld_rb<B, S, NR>(in, K, NTin, j0 + min(i, max(m - 2, 0)), r, Bl);
+    if (i < m - 1) {
+#pragma unroll
+      for (int p = 0; p < NR; ++p) {
+        S tv[B], u[B];
+        if (i == 0) {
+#pragma unroll
+          for (int a = 0; a < B; ++a) tv[a] = yL[p][a];
+        } else {
+          lltsolve<B, S>(Lr[i - 1], Wp[i - 1][p], tv);
         }
-    } else {
 #pragma unroll
-      for (int a = 0; a < B; ++a)
+        for (int a = 0; a < B; ++a) {
+          S acc = r[p][a];
 #pragma unroll
-        for (int q = 0; q < B; ++q) Bs[a][q] = Bl[a][q];
+          for (int q = 0; q < B; ++q) acc = fnma_(Bl[a][q], tv[q], acc);
+          u[a] = acc;
+        }
+        llsolve<B, S>(Lr[i], u, Wp[i][p]);
+      }
     }
   }
-  if (m > 1 && bad_(splat<S>(1.0) / Lc[B - 1][B - 1])) cf = min(cf, 1 + (chunk_begin(j0 + 1, T, K) - 1));
+  S yn[NR][B];
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int a = 0; a < B; ++a) yn[p][a] = yR[p][a];
+#pragma unroll
+  for (int i = MS - 2; i >= 0; --i) {
+    S Bn[B][B];
+    psep_ld_b<B, S, NR>(in, K, j0 + min(i, max(m - 2, 0)) + 1, Bn);  // coupling (j+1, j)
+    if (i < m - 1) {
+#pragma unroll
+      for (int p = 0; p < NR; ++p) {
+        S v[B], u[B], tv[B], yv[B];
+#pragma unroll
+        for (int a = 0; a < B; ++a) {
+          S acc = mul_(Bn[0][a], yn[p][0]);
+#pragma unroll
+          for (int q = 1; q < B; ++q) acc = fma_(Bn[q][a], yn[p][q], acc);
+          v[a] = acc;
+        }
+        llsolve<B, S>(Lr[i], v, u);
+#pragma unroll
+        for (int a = 0; a < B; ++a) tv[a] = sub_(Wp[i][p][a], u[a]);
+        lltsolve<B, S>(Lr[i], tv, yv);
+#pragma unroll
+        for (int a = 0; a < B; ++a) yo[int64_t(p * B + a) * Kout + j0 + i] = yv[a];
+#pragma unroll
+        for (int a = 0; a < B; ++a) yn[p][a] = yv[a];
+      }
+    }
+  }
+}
+
+template <int B, class S, int MS, int NR>
+__global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
+  using BR = BRecN<B, NR>;
+  unsigned char* sm = smnn_dyn_smem;
+  const int K = L.K, nt = blockDim.x;
+  const int t = int(threadIdx.x);
+  const int m = K / nt;  // separators per thread (host: K = m * nt, m <= MS)
+  const int64_t g = blockIdx.x;
+  S* rec = reinterpret_cast<S*>(sm);
+  int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * nt);
+  int* sfail = stime + nt;
+  const int j0 = t * m, js = j0 + m - 1;
+  if (t == 0) sfail[0] = INT_MAX;
+  stime[t] = sep_time(L, js, T);
+  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B, NR>::N) * K;
+  int cf = INT_MAX;
+  for (int j = j0; j <= js; ++j) cf = min(cf, L.cfail[g * K + j]);
+  S Lr[MS - 1][B][B], Ds[B][B], Rs[NR][B], Bs[B][B], All[B][B], rl[NR][B];
+  if (sep_local<B, S, MS, NR>(in, K, L.NT, j0, m, Lr, Ds, Rs, Bs, All, rl)) cf = min(cf, 1 + sep_time(L, j0, T));
   // hand-over (A_ll, r_l, coupling) to super-separator t - 1
   S* pk = rec + t * BR::N;
 #pragma unroll
@@ -405,70 +497,113 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
     rld_v<B, S>(rec + t * BR::N + BR::Y + p * B, yR[p]);
     if (t > 0) rld_v<B, S>(rec + (t - 1) * BR::N + BR::Y + p * B, yL[p]); else zero<B, S>(yL[p]);
   }
-  // ---- recover the owned separators: forward substitution with y_L, back substitution from y_R
   S* yo = reinterpret_cast<S*>(L.ysep) + g * int64_t(NR * B) * K;
-#pragma unroll
-  for (int p = 0; p < NR; ++p)
-#pragma unroll
-    for (int a = 0; a < B; ++a) yo[int64_t(p * B + a) * K + js] = yR[p][a];
-  S Wp[MS - 1][NR][B];
-#pragma unroll
-  for (int i = 0; i < MS - 1; ++i) {
-    S r[NR][B], Bl[B][B];
-    psep_ld_rb<B, S, NR>(in, K, L.NT, j0 + min(i, m - 2), r, Bl);
-    if (i < m - 1) {
-#pragma unroll
-      for (int p = 0; p < NR; ++p) {
-        S tv[B], u[B];
-        if (i == 0) {
-#pragma unroll
-          for (int a = 0; a < B; ++a) tv[a] = yL[p][a];
-        } else {
-          lltsolve<B, S>(Lr[i - 1], Wp[i - 1][p], tv);
-        }
-#pragma unroll
-        for (int a = 0; a < B; ++a) {
-          S acc = r[p][a];
-#pragma unroll
-          for (int q = 0; q < B; ++q) acc = fnma_(Bl[a][q], tv[q], acc);
-          u[a] = acc;
-        }
-        llsolve<B, S>(Lr[i], u, Wp[i][p]);
-      }
-    }
-  }
-  S yn[NR][B];
-#pragma unroll
-  for (int p = 0; p < NR; ++p)
-#pragma unroll
-    for (int a = 0; a < B; ++a) yn[p][a] = yR[p][a];
-#pragma unroll
-  for (int i = MS - 2; i >= 0; --i) {
-    S Bn[B][B];
-    psep_ld_b<B, S, NR>(in, K, j0 + min(i, m - 2) + 1, Bn);  // coupling (j+1, j)
-    if (i < m - 1) {
-#pragma unroll
-      for (int p = 0; p < NR; ++p) {
-        S v[B], u[B], tv[B], yv[B];
-#pragma unroll
-        for (int a = 0; a < B; ++a) {
-          S acc = mul_(Bn[0][a], yn[p][0]);
-#pragma unroll
-          for (int q = 1; q < B; ++q) acc = fma_(Bn[q][a], yn[p][q], acc);
-          v[a] = acc;
-        }
-        llsolve<B, S>(Lr[i], v, u);
-#pragma unroll
-        for (int a = 0; a < B; ++a) tv[a] = sub_(Wp[i][p][a], u[a]);
-        lltsolve<B, S>(Lr[i], tv, yv);
-#pragma unroll
-        for (int a = 0; a < B; ++a) yo[int64_t(p * B + a) * K + j0 + i] = yv[a];
-#pragma unroll
-        for (int a = 0; a < B; ++a) yn[p][a] = yv[a];
-      }
-    }
-  }
+  sep_recover<B, S, MS, NR>(in, K, L.NT, j0, m, Lr, yL, yR, yo, K);
   if (t == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
+}
+
+// ================================================ hierarchical separators ==
+// More separators than one CTA's reduction takes (K > 2048, horizons beyond
+// ~2e4 points): the partition method applied level by level.  Level l holds
+// K_l separator records in the PSep format (P1 writes level 0); SEPL turns
+// them into K_l / 8 super-separator records of level l + 1 (8 separators per
+// thread, 128 threads = 1024 separators per CTA, the A_ll / r_l hand-over
+// through shared memory inside a CTA and through the record's AL / RL fields
+// across CTAs, exactly as P1 does); the top level (<= 2048) is solved by
+// pipe_sep2_kernel; SEPR recovers level l's y from level l + 1's (re-doing the
+// local elimination for its factors).  Every level's system is the Schur
+// complement of the one below: the result equals the one-level solve up to
+// rounding (block Cholesky of a permuted system).
+constexpr int kSepLM = 8, kSepLNT = 128;
+
+template <int B, class S, int NR>
+__global__ void __launch_bounds__(kSepLNT, 2) pipe_sepl_kernel(PipeL L, PipeL U, int T) {
+  using Q = PSep<B, NR>;
+  constexpr int LT = B * (B + 1) / 2, HN = LT + NR * B;
+  __shared__ S ho[HN * kSepLNT];
+  const int K = L.K, Ku = U.K;  // Ku = K / 8
+  const int parts = K / (kSepLM * kSepLNT);
+  const int64_t g = blockIdx.x / parts;
+  const int c = int(blockIdx.x % parts), t = int(threadIdx.x);
+  const int su = c * kSepLNT + t;  // this thread's super-separator (level l + 1)
+  const int j0 = su * kSepLM;
+  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(Q::N) * K;
+  int cf = INT_MAX;
+  for (int j = j0; j < j0 + kSepLM; ++j) cf = min(cf, L.cfail[g * K + j]);
+  S Lr[kSepLM - 1][B][B], Ds[B][B], Rs[NR][B], Bs[B][B], All[B][B], rl[NR][B];
+  if (sep_local<B, S, kSepLM, NR>(in, K, L.NT, j0, kSepLM, Lr, Ds, Rs, Bs, All, rl)) cf = min(cf, 1 + sep_time(L, j0, T));
+  int e = 0;
+#pragma unroll
+  for (int a = 0; a < B; ++a)
+#pragma unroll
+    for (int q = 0; q <= a; ++q) ho[(e++) * kSepLNT + t] = neg_(All[a][q]);
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int a = 0; a < B; ++a) ho[(LT + p * B + a) * kSepLNT + t] = neg_(rl[p][a]);
+  __syncthreads();
+  if (t + 1 < kSepLNT) {
+    e = 0;
+#pragma unroll
+    for (int a = 0; a < B; ++a)
+#pragma unroll
+      for (int q = 0; q <= a; ++q) Ds[a][q] = add_(Ds[a][q], ho[(e++) * kSepLNT + t + 1]);
+#pragma unroll
+    for (int p = 0; p < NR; ++p)
+#pragma unroll
+      for (int a = 0; a < B; ++a) Rs[p][a] = add_(Rs[p][a], ho[(LT + p * B + a) * kSepLNT + t + 1]);
+  }
+  S* o = reinterpret_cast<S*>(U.sep1) + g * int64_t(Q::N) * Ku + su;
+  e = 0;
+#pragma unroll
+  for (int a = 0; a < B; ++a)
+#pragma unroll
+    for (int q = 0; q <= a; ++q) o[int64_t(Q::D + e++) * Ku] = Ds[a][q];
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int a = 0; a < B; ++a) o[int64_t(Q::R + p * B + a) * Ku] = Rs[p][a];
+#pragma unroll
+  for (int a = 0; a < B; ++a)
+#pragma unroll
+    for (int q = 0; q < B; ++q) o[int64_t(Q::BL + a * B + q) * Ku] = Bs[a][q];
+  if (t == 0 && su > 0) {  // the previous CTA's last super-separator adds these (psep_ld, NT = 128)
+    e = 0;
+#pragma unroll
+    for (int a = 0; a < B; ++a)
+#pragma unroll
+      for (int q = 0; q <= a; ++q) o[int64_t(Q::AL + e++) * Ku] = neg_(All[a][q]);
+#pragma unroll
+    for (int p = 0; p < NR; ++p)
+#pragma unroll
+      for (int a = 0; a < B; ++a) o[int64_t(Q::RL + p * B + a) * Ku] = neg_(rl[p][a]);
+  }
+  U.cfail[g * Ku + su] = cf;
+}
+
+template <int B, class S, int NR>
+__global__ void __launch_bounds__(kSepLNT, 2) pipe_sepr_kernel(PipeL L, PipeL U) {
+  using Q = PSep<B, NR>;
+  const int K = L.K, Ku = U.K;
+  const int parts = K / (kSepLM * kSepLNT);
+  const int64_t g = blockIdx.x / parts;
+  const int c = int(blockIdx.x % parts), t = int(threadIdx.x);
+  const int su = c * kSepLNT + t;
+  const int j0 = su * kSepLM;
+  const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(Q::N) * K;
+  S Lr[kSepLM - 1][B][B], Ds[B][B], Rs[NR][B], Bs[B][B], All[B][B], rl[NR][B];
+  sep_local<B, S, kSepLM, NR>(in, K, L.NT, j0, kSepLM, Lr, Ds, Rs, Bs, All, rl);  // factors only
+  const S* yu = reinterpret_cast<const S*>(U.ysep) + g * int64_t(NR * B) * Ku;
+  S yL[NR][B], yR[NR][B];
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+#pragma unroll
+    for (int a = 0; a < B; ++a) {
+      yR[p][a] = yu[int64_t(p * B + a) * Ku + su];
+      yL[p][a] = su > 0 ? yu[int64_t(p * B + a) * Ku + su - 1] : splat<S>(0.0);
+    }
+  S* yo = reinterpret_cast<S*>(L.ysep) + g * int64_t(NR * B) * K;
+  sep_recover<B, S, kSepLM, NR>(in, K, L.NT, j0, kSepLM, Lr, yL, yR, yo, K);
 }
 
 

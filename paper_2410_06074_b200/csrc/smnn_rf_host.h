@@ -76,6 +76,7 @@ size_t pipe_workspace_bytes(const smnn_problem* p);
 // Whether rf_launch / pipe_launch would take the problem (no launch).
 bool rf_eligible(const smnn_problem* p, bool bwd);
 bool pipe_eligible(const smnn_problem* p, bool bwd);
+int pipe_launches(const smnn_problem* p, bool bwd);  // 3 + 2 per separator-hierarchy level
 
 // Cluster-resident fp64-arithmetic path (smnn_x64.cu): SMNN_F32_C64 and
 // SMNN_F64 while one cluster of <= 16 CTAs holds an instance.  Same contract

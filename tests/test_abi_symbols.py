@@ -73,7 +73,9 @@ def test_kernel_path_selection(lib):
     assert kernel_path(4096, 10000, 2, 2, compute="f64", bwd=True) == "pipe"
     assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64) == "pipe"
     assert kernel_path(1536, 1000, 2, 2, dtype=torch.float64, path="x64") == "x64"
-    assert kernel_path(64, 100000, 2, 2, dtype=torch.float64) == "checkpoint"  # > 2048 separators
+    assert kernel_path(64, 100000, 2, 2, dtype=torch.float64) == "pipe"  # separator hierarchy
+    assert kernel_path(64, 1000000, 2, 2, compute="f64", bwd=True) == "pipe"
+    assert kernel_path(2, 20000000, 2, 2, dtype=torch.float64) == "checkpoint"  # beyond 3 levels
     assert kernel_path(2, 3, 2, 2) == "checkpoint"                    # too short to chunk
     assert kernel_path(1536, 1000, 2, 2, compute="f64", path="pipe") == "pipe"
     assert kernel_path(1536, 1000, 2, 2, path="x64") == "rf"          # x64 needs fp64 arithmetic: fallback
@@ -97,7 +99,9 @@ def test_launch_count(lib):
     assert count(10000, _abi.SMNN_F32_C64, 1) == 3                       # pipeline, re-solves y itself
     assert count(1000, _abi.SMNN_F32_C64, 1, path=_abi.SMNN_PATH_X64) == 1  # x64 re-solves y itself
     assert count(1000, _abi.SMNN_F32_C64, 1, path=_abi.SMNN_PATH_PIPE) == 3     # re-solves y (2 rhs)
-    assert count(100000, _abi.SMNN_F32_C64, 1) == 5 + 1 + 1 + 4 + 1      # checkpoint kernels, promoted
+    assert count(100000, _abi.SMNN_F32_C64, 1) == 3 + 2                  # pipeline, 1 separator level
+    assert count(1000000, _abi.SMNN_F64, 0) == 3 + 2 * 2                 # pipeline, 2 separator levels
+    assert count(20000000, _abi.SMNN_F32_C64, 1, n=2) == 5 + 1 + 1 + 4 + 1  # checkpoint kernels, promoted
 
 
 def test_workspace_covers_promotion(lib):
@@ -105,7 +109,7 @@ def test_workspace_covers_promotion(lib):
     the inputs, dl/dy, y and the gradients (9 [n, T, b]-sized or smaller arrays)
     plus the fp64 path's own workspace."""
     from paper_2410_06074_b200 import _abi
-    n, T = 64, 100000
+    n, T = 2, 20000000
     p = _abi.smnn_problem(n_inst=n, T=T, order=2, n_iv=2, dtype=_abi.SMNN_F32_C64, threads_per_inst=0, path=0,
                           w_gov=1, w_init=1, w_smooth=1)
     q = _abi.smnn_problem(n_inst=n, T=T, order=2, n_iv=2, dtype=_abi.SMNN_F64, threads_per_inst=0, path=0,

@@ -295,6 +295,7 @@ def test_host_plan_rejects_bad_buffers(smnn):
 PATH_CASES = [  # (n, T, R, n_iv): every kernel path must match the oracle, forced through smnn_problem.path
     (3, 64, 2, 2), (2, 1000, 2, 2), (2, 777, 1, 1), (2, 3000, 2, 2), (2, 257, 3, 4), (2, 400, 0, 1),
     (3, 20, 2, 2), (2, 9, 1, 1), (2, 40, 3, 3), (2, 1461, 2, 2),
+    (2, 30000, 2, 2), (2, 41000, 3, 3),  # beyond 2048 separators: the pipeline's separator hierarchy
 ]
 
 
