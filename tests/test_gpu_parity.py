@@ -91,16 +91,48 @@ def to_dev(x, dtype):
     return {k: torch.from_numpy(np.asarray(v)).to("cuda", dtype) for k, v in x.items()}
 
 
+_KAPPA = {}
+
+
 def kappa(x, i, w):
+    """kappa(M) of instance i: dense eigenvalues for small systems; else the largest
+    eigenvalue by power iteration and the smallest by inverse iteration on the
+    banded Cholesky factor (Rayleigh quotients: kappa is not overestimated, the
+    kappa-aware bounds only get stricter).  Memoised per input array."""
+    import hashlib
+    key = (hashlib.sha1(np.ascontiguousarray(x["coeffs"][i]).tobytes()
+                        + np.ascontiguousarray(x["steps"][i]).tobytes()).hexdigest(), tuple(w))
+    if key in _KAPPA:
+        return _KAPPA[key]
     p = O.instance_problem(x["coeffs"].shape[1], x["coeffs"].shape[2] - 1, x["iv"].shape[1], *w)
     M, _ = O.normal_matrix_sparse(p, *O.instance_to_general(x["coeffs"][i], x["rhs"][i], x["iv"][i],
                                                             x["steps"][i]))
     if M.shape[0] <= 600:
         ev = np.linalg.eigvalsh(M.toarray())
-        return ev[-1] / ev[0]
-    lmax = scipy.sparse.linalg.eigsh(M, k=1, which="LA", return_eigenvectors=False)[0]
-    lmin = scipy.sparse.linalg.eigsh(M, k=1, sigma=0, which="LM", return_eigenvectors=False)[0]
-    return lmax / lmin
+        k = ev[-1] / ev[0]
+    else:
+        import scipy.linalg as sl
+        b = x["coeffs"].shape[2]
+        bw = 2 * b - 1
+        n = M.shape[0]
+        ab = np.zeros((bw + 1, n))
+        C = M.tocoo()  # lower band storage: ab[d, j] = M[j + d, j]
+        sel = (C.row >= C.col) & (C.row - C.col <= bw)
+        ab[C.row[sel] - C.col[sel], C.col[sel]] = C.data[sel]
+        cb = sl.cholesky_banded(ab, lower=True)
+        v = np.random.default_rng(0).standard_normal(n)
+        for _ in range(60):
+            v = sl.cho_solve_banded((cb, True), v)
+            v /= np.linalg.norm(v)
+        lmin = float(v @ (M @ v))
+        u = np.random.default_rng(1).standard_normal(n)
+        for _ in range(100):  # power iteration (Rayleigh quotient: a lower bound on lambda_max)
+            u = M @ u
+            u /= np.linalg.norm(u)
+        lmax = float(u @ (M @ u))
+        k = lmax / lmin
+    _KAPPA[key] = k
+    return k
 
 
 def backward_error(x, y, i, w):
@@ -307,12 +339,14 @@ def test_forced_kernel_paths(smnn, path, n, T, R, n_iv, mode):
     forced through smnn_problem.path, against the oracle: y and all gradients.
     A forced path that does not fit the shape falls back (the reported path is
     checked against the request when it is eligible)."""
+    tdt, compute = MODES[mode]
+    got = smnn.kernel_path(n, T, R, n_iv, tdt, compute, w=smnn.Weights(*W), path=path)
+    if T > 5000 and {"resident": "checkpoint", "stream": "checkpoint"}.get(path, path) != got:
+        pytest.skip(f"{path} does not take T = {T}; the fallback ({got}) runs under its own name")
     x = inputs_in(make_inputs(n, T, R, n_iv, dtype="f64", seed=3 * T + R), mode)
     gy = make_grad_y(n, T, R, dtype="f64" if mode == "f64" else "f32", seed=T + 5)
     y_ref, g_ref = oracle_refs(x, gy, np.arange(n), w=W, workers=1)
     y, g = run(smnn, x, gy, mode, smnn.Weights(*W), path=path)
-    tdt, compute = MODES[mode]
-    got = smnn.kernel_path(n, T, R, n_iv, tdt, compute, w=smnn.Weights(*W), path=path)
     e = errors(y, g, y_ref, g_ref)
     rec = dict(path=path, ran=got, mode=mode, n=n, T=T, R=R, err=e)
     if mode == "f32c64":
@@ -377,12 +411,13 @@ def test_full_size_f32(smnn, name):
     log("full_size_f32", workload=name, kappa=kap, err=e)
 
 
+_CORNER_INPUTS = {}
 CORNERS = {  # configs[4] scaling-sweep corners: workload -> instances checked against the oracle
     "sweep_t1e2": 16, "sweep_wide": 16, "sweep_t1e5": 3, "sweep_t1e6": 2, "sweep_o3_t1e5": 2,
 }
 
 
-@pytest.mark.parametrize("mode", ["f32c64", "f64"])
+@pytest.mark.parametrize("mode", ["f32c64", "f64"])  # the top decorator varies fastest: one input set per name
 @pytest.mark.parametrize("name", list(CORNERS))
 def test_scaling_sweep_corners(smnn, name, mode):
     """BASELINE.json configs[4] corners (T = 1e2 .. 1e6, B*D up to 65536, order 2 and
@@ -390,9 +425,13 @@ def test_scaling_sweep_corners(smnn, name, mode):
     finite everywhere; sampled instances against the oracle -- f32c64 hard 1e-4
     on y and all gradients, f64 hard 1e-9 at order 2 (order 3: kappa bound)."""
     wl = workload(name)
-    st = "f64" if mode == "f64" else "f32"
-    x = make_workload_inputs(wl.with_(dtype=st), seed=5)
-    gy = make_grad_y(wl.n_inst, wl.T, wl.order, dtype=st, seed=6)
+    if name not in _CORNER_INPUTS:  # generated once (fp64), rounded per mode
+        _CORNER_INPUTS.clear()
+        _CORNER_INPUTS[name] = (make_workload_inputs(wl.with_(dtype="f64"), seed=5),
+                                make_grad_y(wl.n_inst, wl.T, wl.order, dtype="f64", seed=6))
+    x64, gy64 = _CORNER_INPUTS[name]
+    x = inputs_in(x64, mode)
+    gy = gy64 if mode == "f64" else gy64.astype(np.float32)
     idx = np.linspace(0, wl.n_inst - 1, CORNERS[name]).astype(int)
     y_ref, g_ref = oracle_refs(x, gy, idx, chunk=1)
     y, g = run(smnn, x, gy, mode)
