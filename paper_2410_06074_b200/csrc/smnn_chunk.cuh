@@ -347,115 +347,13 @@ __device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, in
   }
 }
 
-// p2_seg with the stored segment's factors and forward-substituted right-hand
-// sides in a per-thread shared-memory scratch instead of registers (scr:
-// this thread's base, fields strided by `st`): both sweeps are rolled loops,
-// so the kernel's code stays small (the register version of the fp64 NR = 2
-// backward is ~8k instructions and stalls on instruction fetch).
-template <int B, class Tio, class S, bool BWD, int HM, int NR>
-__device__ __forceinline__ void p2_seg_smem(const Grp<Tio, 1>& x, const Wts<S>& w, int k, int f, int i0, int len,
-                                            const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS,
-                                            const S (&yL)[NR][B], S (&Ls)[B][B], S (&ws)[NR][B], S (&yn)[NR][B],
-                                            S (&yfn)[B], S* scr, int st) {
-  constexpr int LT = B * (B + 1) / 2, FN = LT + NR * B;  // scratch values per point
-  S ap[2 * B - 1];
-  if (i0 > 0 || k > 0) spow<B, S>(S(sS[i0 - 1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
-#pragma unroll 1
-  for (int q = 0; q < len; ++q) {
-    const int i = i0 + q;
-    S c[B], an[2 * B - 1], M[B][B], wc[B], rhs[NR][B];
-#pragma unroll
-    for (int r = 0; r < B; ++r) c[r] = S(cS[i * B + r]);
-    spow<B, S>(S(sS[i]), w.s2, an);
-    lassemble<B, S>(c, w.g2, ap, an, M, wc);
-    const bool t0 = i == 0 && k == 0;
-    chunk_rhs<B, Tio, S, BWD, NR>(w, x.n_iv, x.u[0], t0, wc, dS, gS, i, rhs);
-    if (i == 0) {
-      if (t0) {
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-          if (r < x.n_iv) M[r][r] = add_(M[r][r], w.i2);
-      }
-#pragma unroll
-      for (int p = 0; p < NR; ++p) {
-        S Nt[B];
-        rNv<B, S>(ap, yL[p], Nt);
-#pragma unroll
-        for (int r = 0; r < B; ++r) rhs[p][r] = sub_(rhs[p][r], Nt[r]);
-      }
-    } else {
-      S Pm[B][B];
-      lPfromN<B, S>(ap, Ls, Pm);
-      lcouple<B, S>(Pm, ws[0], M, rhs[0]);
-#pragma unroll
-      for (int p = 1; p < NR; ++p) lcouple_v<B, S>(Pm, ws[p], rhs[p]);
-    }
-    lchol<B, S>(M, Ls);
-#pragma unroll
-    for (int p = 0; p < NR; ++p) llsolve<B, S>(Ls, rhs[p], ws[p]);
-    S* o = scr + q * FN * st;
-    int e = 0;
-#pragma unroll
-    for (int r = 0; r < B; ++r)
-#pragma unroll
-      for (int c2 = 0; c2 <= r; ++c2) o[(e++) * st] = Ls[r][c2];
-#pragma unroll
-    for (int p = 0; p < NR; ++p)
-#pragma unroll
-      for (int r = 0; r < B; ++r) o[(LT + p * B + r) * st] = ws[p][r];
-#pragma unroll
-    for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
-  }
-#pragma unroll 1
-  for (int q = len - 1; q >= 0; --q) {
-    const int i = i0 + q, j = f + i;
-    const S* o = scr + q * FN * st;
-    S Lq[B][B], an[2 * B - 1], yv[NR][B];
-    int e = 0;
-#pragma unroll
-    for (int r = 0; r < B; ++r)
-#pragma unroll
-      for (int c2 = 0; c2 <= r; ++c2) Lq[r][c2] = o[(e++) * st];
-    spow<B, S>(S(sS[i]), w.s2, an);
-#pragma unroll
-    for (int p = 0; p < NR; ++p) {
-      S v[B], uu[B], t[B];
-      rNtv<B, S>(an, yn[p], v);
-      llsolve<B, S>(Lq, v, uu);
-#pragma unroll
-      for (int r = 0; r < B; ++r) t[r] = sub_(o[(LT + p * B + r) * st], uu[r]);
-      lltsolve<B, S>(Lq, t, yv[p]);
-    }
-    if (!BWD) {
-#pragma unroll
-      for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[0][r]);
-    } else {
-      S yf[B];
-      if (NR == 2) {
-#pragma unroll
-        for (int r = 0; r < B; ++r) yf[r] = yv[NR - 1][r];
-      } else {
-        ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
-      }
-      lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv[0], yf);
-      if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv[0], yf, yn[0], yfn));
-#pragma unroll
-      for (int r = 0; r < B; ++r) yfn[r] = yf[r];
-    }
-#pragma unroll
-    for (int p = 0; p < NR; ++p)
-#pragma unroll
-      for (int r = 0; r < B; ++r) yn[p][r] = yv[p][r];
-  }
-}
-
 // Pass 2 of one chunk with y_L = y(sigma_{k-1}) and y_R = y(sigma_k) known
 // (NR right-hand sides): outputs at the separator, then the interior in (at
 // most) two register segments (p2_seg).
-template <int B, class Tio, class S, bool BWD, int CM, int NR = 1, bool SMR = false>
+template <int B, class Tio, class S, bool BWD, int CM, int NR = 1>
 __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, int k, int f, int sig, int nint,
                                          const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS,
-                                         const S (&yL)[NR][B], const S (&yR)[NR][B], S* scr = nullptr, int st = 0) {
+                                         const S (&yL)[NR][B], const S (&yR)[NR][B]) {
   // a chunk longer than HM is split as [0, h) + [h, nint) with the second
   // segment HM long; [0, h) is factored twice (run-through to reach the state
   // at h - 1, then stored for its back substitution).
@@ -483,19 +381,7 @@ __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, 
     }
     lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR[0], yfn);
   }
-  if constexpr (SMR) {  // stored segments in the shared-memory scratch (HM points each)
-    if (CM - 1 <= HM || nint <= HM) {
-      p2_seg_smem<B, Tio, S, BWD, HM, NR>(x, w, k, f, 0, nint, cS, dS, sS, gS, yL, Ls, ws, yn, yfn, scr, st);
-    } else {
-      const int h = nint - HM;
-      p2_seg<B, Tio, S, BWD, HM, false, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
-      p2_seg_smem<B, Tio, S, BWD, HM, NR>(x, w, k, f, h, HM, cS, dS, sS, gS, yL, Ls, ws, yn, yfn, scr, st);
-      zero<B, S>(Ls);
-#pragma unroll
-      for (int p = 0; p < NR; ++p) zero<B, S>(ws[p]);
-      p2_seg_smem<B, Tio, S, BWD, HM, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, yL, Ls, ws, yn, yfn, scr, st);
-    }
-  } else if (CM - 1 <= HM || nint <= HM) {
+  if (CM - 1 <= HM || nint <= HM) {
     p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, 0, nint, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
   } else {
     // (measured: calling one stored-segment copy twice from a rolled loop

@@ -24,10 +24,6 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 #define SMNN_PIPE_M8_64 (1 << 30)
 #endif
 
-#ifndef SMNN_P2_SMEM_KB  // chunk-kernel CTAs shrink while P2's staged range exceeds this
-#define SMNN_P2_SMEM_KB 64
-#endif
-
 template <int B>
 size_t nr_sep_fields(int nr) { return nr == 2 ? size_t(PSep<B, 2>::N) : size_t(PSep<B, 1>::N); }
 
@@ -109,8 +105,6 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     L.off_g = bwd ? take(size_t(steps) * B * es + 32) : 0;
     L.off_y = (bwd && p2 && nr == 1) ? take(size_t(steps) * B * es + 32) : 0;
     L.off_h = p2 ? 0 : take(size_t(PSep<B>::LT + nr * B) * SMNN_PIPE_NT * ls);
-    L.off_scr = (p2 && SMNN_P2_SMR && sizeof(S) >= 8)
-                    ? take(size_t(PipeHM<B, S>::value) * (PSep<B>::LT + nr * B) * q.NT * ls) : 0;
     L.off_bar = take(16);
     return off;
   };
@@ -121,7 +115,7 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     steps = q.NT * CM + 2;  // points of one CTA range (+ s_{ta-1}, y_{ta-1})
     q.smem_p1 = layout(q.L1, false);
     q.smem_p2 = layout(q.L2, true);
-    if (q.NT <= 32 || (q.smem_p1 <= 64 * 1024 && q.smem_p2 <= SMNN_P2_SMEM_KB * 1024)) break;
+    if (q.NT <= 32 || std::max(q.smem_p1, q.smem_p2) <= 64 * 1024) break;
     q.NT /= 2;
   }
   q.parts = (K + q.NT - 1) / q.NT;
@@ -206,7 +200,7 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   auto chain = [&](cudaStream_t s) {
     PipeL L1 = level(0), L2 = level(0);
     L2.off_c = q.L2.off_c; L2.off_d = q.L2.off_d; L2.off_s = q.L2.off_s; L2.off_g = q.L2.off_g;
-    L2.off_y = q.L2.off_y; L2.off_h = q.L2.off_h; L2.off_bar = q.L2.off_bar; L2.off_scr = q.L2.off_scr;
+    L2.off_y = q.L2.off_y; L2.off_h = q.L2.off_h; L2.off_bar = q.L2.off_bar;
     k1<<<unsigned(n * q.parts), q.NT, q.smem_p1, s>>>(a, L1);
     for (int l = 0; l < q.levels; ++l)
       pipe_sepl_kernel<B, S, NR><<<unsigned(n * (q.Kl[l] / (kSepLM * kSepLNT))), kSepLNT, 0, s>>>(level(l), level(l + 1),

@@ -63,11 +63,6 @@ namespace smnn {
 #ifndef SMNN_PIPE_P1_MINB64
 #define SMNN_PIPE_P1_MINB64 3
 #endif
-// fp64 arithmetic: P2's stored segments in shared memory (rolled loops, small
-// code) instead of registers (fully unrolled)
-#ifndef SMNN_P2_SMR
-#define SMNN_P2_SMR 0
-#endif
 #ifndef SMNN_PIPE_SEP_MAX
 #define SMNN_PIPE_SEP_MAX 2048
 #endif
@@ -79,7 +74,6 @@ struct PipeL {
   int NT;         // threads per CTA of the chunk kernels
   int parts;      // CTAs per instance of the chunk kernels
   int off_c, off_d, off_s, off_g, off_y, off_h, off_bar;  // shared-memory byte offsets (16-aligned)
-  int off_scr;    // P2 with SMNN_P2_SMR: per-thread factor scratch (fp64 arithmetic)
   void* sep1;
   void* ysep;
   int* cfail;
@@ -689,9 +683,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? (NR == 2
   __syncthreads();  // barrier initialised
   mbar_wait(bar, 0);
 
-  constexpr bool SMR = SMNN_P2_SMR && sizeof(S) >= 8;
-  S* scr = reinterpret_cast<S*>(sm + L.off_scr) + tid;
-  if (act) p2_chunk<B, Tio, S, BWD, CM, NR, SMR>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR, scr, blockDim.x);
+  if (act) p2_chunk<B, Tio, S, BWD, CM, NR>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR);
   // ---- outputs: TMA bulk store of the aligned body, plain stores at the ends
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
