@@ -6,6 +6,7 @@ import os
 import shutil
 import subprocess
 import sys
+import time
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -67,6 +68,7 @@ def build_library(force: bool = False, verbose: bool = False, extra=()) -> str:
     flags = [f for f in NVCC_FLAGS if f != "-shared"]
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     procs, objs = [], []
+    t_start = time.time()  # objects are stamped with this: a source edited during the compile stays newer
     for s in SOURCES:
         obj = _obj(s)
         objs.append(obj)
@@ -81,6 +83,8 @@ def build_library(force: bool = False, verbose: bool = False, extra=()) -> str:
         out, err = pr.communicate()
         if pr.returncode != 0:
             errs.append(" ".join(cmd) + "\n" + out + err)
+        else:
+            os.utime(cmd[cmd.index("-o") + 1], (t_start, t_start))
     if errs:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
