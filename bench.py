@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threads-per-inst", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ylo", action="store_true",
+                    help="f32c64: backward re-solves y (two right-hand sides) instead of reading the forward's "
+                         "fp32 remainder y_lo")
     ap.add_argument("--e2e-steps", type=int, default=10)
     return ap.parse_args()
 
@@ -250,6 +253,7 @@ def main():
     n_local = sdist.shard_range(wl.n_inst, rank, world)[1] - sdist.shard_range(wl.n_inst, rank, world)[0] \
         if shard else wl.n_inst
     ev_stream = torch.cuda.current_stream(dev)
+    use_ylo = compute == "f64" and not args.no_ylo and smnn.ylo_used(t["coeffs"], t["iv"], w, compute, tpi)
 
     def step(ev=None):
         if shard:
@@ -257,10 +261,15 @@ def main():
             return y_all, g[4], g
         if ev:
             ev[0].record(ev_stream)
-        y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi)
+        y_lo = None
+        if use_ylo:  # f32c64 on the pipeline: the forward hands the backward y's fp32 remainder
+            y, info, y_lo = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi,
+                                                       with_ylo=True)
+        else:
+            y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi)
         if ev:
             ev[1].record(ev_stream)
-        g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, w, compute, tpi)
+        g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, w, compute, tpi, y_lo=y_lo)
         if ev:
             ev[2].record(ev_stream)
         return y, info, g
@@ -385,7 +394,9 @@ def main():
             "config": {"workload": wl.name, "desc": wl.desc, "B": wl.B, "D": wl.D, "T": wl.T, "order": wl.order,
                        "instances_per_gpu": n_local, "storage": store, "arithmetic": arith,
                        "mode": args.dtype + (" (verified to 1e-4 on y and all gradients, tests/test_gpu_parity.py)"
-                                             if args.dtype == "f32c64" else ""),
+                                             if args.dtype == "f32c64" else "")
+                               + (" + y_lo: the backward reads the forward's fp32 remainder of y (smnn_*_ex)"
+                                  if use_ylo else ""),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "parallelism": (f"shard{world}: one batch split over {world} ranks, y all_gather + loss "
                                        f"all_reduce (NCCL) inside the step") if shard else

@@ -147,6 +147,30 @@ int smnn_solve_bwd(const smnn_problem* p, const void* coeffs, const void* rhs,
                    void* grad_coeffs, void* grad_rhs, void* grad_iv, void* grad_steps,
                    int32_t* info, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same two calls with the fp32 REMAINDER of y (SMNN_F32_C64 only).
+ * The f32c64 forward computes y in fp64 and rounds it into the fp32 `y`; with
+ * y_lo (device, [n_inst, T, b] float, nullable) it also writes
+ * y_lo = fl32(y_fp64 - (double)y), so that (double)y + (double)y_lo carries
+ * the fp64 solution to ~2^-48 relative.  smnn_solve_bwd_ex given that pair
+ * reads y = y + y_lo in fp64 for the gradient chain (Algorithm 2's
+ * dl/dM = -dl/dbeta y^T and the residual terms of Appendix A.1), instead of
+ * re-solving y beside dl/dbeta: one right-hand side instead of two (the
+ * same gradients up to rounding).  The pair is used only where
+ * smnn_ylo_used(p) returns 1 (both directions on the pipeline); otherwise
+ * the forward fills y_lo with zeros and the backward ignores it (y is then
+ * re-solved as in smnn_solve_bwd).  For SMNN_F32 / SMNN_F64 y_lo must be
+ * NULL-or-ignored: it is not read or written.  A y_lo that does not come
+ * from the forward of the same inputs gives wrong gradients (not detected). */
+int smnn_ylo_used(const smnn_problem* p);
+int smnn_factor_solve_fwd_ex(const smnn_problem* p, const void* coeffs, const void* rhs,
+                             const void* iv, const void* steps, void* y, void* y_lo, int32_t* info,
+                             void* workspace, size_t workspace_bytes, void* stream);
+int smnn_solve_bwd_ex(const smnn_problem* p, const void* coeffs, const void* rhs,
+                      const void* iv, const void* steps, const void* y, const void* y_lo,
+                      const void* grad_y, void* grad_coeffs, void* grad_rhs, void* grad_iv,
+                      void* grad_steps, int32_t* info, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
 /* Algorithm 3 "Decompose", materialised: one sequential
  * sweep per instance writing L [n,T,b,b] and P [n,T-1,b,b] to HBM (the
  * paper's own data flow; used for parity and as the sequential baseline).

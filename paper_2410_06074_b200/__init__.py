@@ -7,7 +7,7 @@ helpers (``dist``).  It never imports ``oracle/``.
 
 from .smnn import (  # noqa: F401
     HostPlan, SMNNSolve, Weights, smnn_assemble, smnn_factor, smnn_factor_solve_fwd, smnn_solve,
-    smnn_solve_bwd, smnn_substitute, workspace_bytes, kernel_path,
+    smnn_solve_bwd, smnn_substitute, workspace_bytes, kernel_path, ylo_used,
 )
 
 __version__ = "0.1.0"

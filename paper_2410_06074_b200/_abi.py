@@ -16,7 +16,7 @@ EXPORTED = [
     "smnn_version", "smnn_last_error", "smnn_workspace_bytes", "smnn_assemble",
     "smnn_factor_solve_fwd", "smnn_solve_bwd", "smnn_factor", "smnn_substitute",
     "smnn_plan_create", "smnn_plan_destroy", "smnn_plan_fwd_bwd_host", "smnn_kernel_path",
-    "smnn_launch_count",
+    "smnn_launch_count", "smnn_ylo_used", "smnn_factor_solve_fwd_ex", "smnn_solve_bwd_ex",
 ]
 SMNN_PATH_RF, SMNN_PATH_PIPE, SMNN_PATH_CHECKPOINT, SMNN_PATH_X64, SMNN_PATH_STREAM = 1, 2, 3, 4, 5
 PATH_NAMES = {1: "rf", 2: "pipe", 3: "checkpoint", 4: "x64"}
@@ -77,6 +77,12 @@ def load(build_if_missing: bool = False, path: str | None = None) -> ctypes.CDLL
     L.smnn_factor_solve_fwd.argtypes = [PP, P, P, P, P, P, I32P, P, ctypes.c_size_t, P]
     L.smnn_solve_bwd.restype = ctypes.c_int
     L.smnn_solve_bwd.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, I32P, P, ctypes.c_size_t, P]
+    L.smnn_ylo_used.restype = ctypes.c_int
+    L.smnn_ylo_used.argtypes = [PP]
+    L.smnn_factor_solve_fwd_ex.restype = ctypes.c_int
+    L.smnn_factor_solve_fwd_ex.argtypes = [PP, P, P, P, P, P, P, I32P, P, ctypes.c_size_t, P]
+    L.smnn_solve_bwd_ex.restype = ctypes.c_int
+    L.smnn_solve_bwd_ex.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, P, I32P, P, ctypes.c_size_t, P]
     L.smnn_factor.restype = ctypes.c_int
     L.smnn_factor.argtypes = [PP, P, P, P, P, I32P, P]
     L.smnn_substitute.restype = ctypes.c_int

@@ -231,6 +231,32 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
   return bad;
 }
 
+// y at point j for the backward gradient chain: the staged fp32 (or fp64) y,
+// plus, in the SMNN_F32_C64 pipeline, the forward's fp32 remainder y_lo (staged)
+// so that y_hi + y_lo carries the fp64 solution (include/smnn.h smnn_solve_bwd_ex).
+template <int B, class S, class Tio>
+__device__ __forceinline__ void ld_yfwd(const Grp<Tio, 1>& x, int j, S (&yf)[B]) {
+  ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
+  if constexpr (sizeof(S) > sizeof(Tio)) {
+    if (x.ylo_in) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) yf[r] = add_(yf[r], S(smem_as<const Tio>()[x.ylo_off + j * B + r]));
+    }
+  }
+}
+// y at point j in the forward: rounded to storage, and its fp32 remainder when requested.
+template <int B, class S, class Tio>
+__device__ __forceinline__ void st_yout(const Grp<Tio, 1>& x, int j, const S (&y)[B]) {
+#pragma unroll
+  for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, y[r]);
+  if constexpr (sizeof(S) > sizeof(Tio)) {
+    if (x.ylo_out) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) smem_as<Tio>()[x.ylo_off + j * B + r] = Tio(sub_(y[r], S(Tio(y[r]))));
+    }
+  }
+}
+
 // One segment [i0, i0 + len) of a chunk interior (len <= HM) in pass 2: forward
 // sweep re-factoring M from the state (Ls, ws) = (L, w') at step i0 - 1 (from
 // the chunk start -- initial-value rows, rhs -= N_{f-1} y_L -- when i0 == 0),
@@ -324,15 +350,14 @@ __device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, in
         lltsolve<B, S>(Lr[STORE ? q : 0], t, yv[p]);
       }
       if (!BWD) {
-#pragma unroll
-        for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, j * B + r, yv[0][r]);
+        st_yout<B, S, Tio>(x, j, yv[0]);
       } else {
         S yf[B];  // y at j: re-solved (NR = 2) or read from storage
         if (NR == 2) {
 #pragma unroll
           for (int r = 0; r < B; ++r) yf[r] = yv[NR - 1][r];
         } else {
-          ldlv<B, S, Tio, 1, true>(x.yin, j * B, yf);
+          ld_yfwd<B, S, Tio>(x, j, yf);
         }
         lpoint_grads<B, S, Tio, 1, true>(x, w, j, yv[0], yf);
         if (x.gs.on) stl<S, Tio, 1, true>(x.gs, 1, j, lds<B, S>(an, yv[0], yf, yn[0], yfn));
@@ -370,14 +395,13 @@ __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, 
   zero<B, S>(yfn);
   zero<B, S>(Ls);
   if (!BWD) {
-#pragma unroll
-    for (int r = 0; r < B; ++r) stl<S, Tio, 1, true>(x.yout, 1, sig * B + r, yR[0][r]);
+    st_yout<B, S, Tio>(x, sig, yR[0]);
   } else {
     if (NR == 2) {
 #pragma unroll
       for (int r = 0; r < B; ++r) yfn[r] = yR[NR - 1][r];
     } else {
-      ldlv<B, S, Tio, 1, true>(x.yin, sig * B, yfn);
+      ld_yfwd<B, S, Tio>(x, sig, yfn);
     }
     lpoint_grads<B, S, Tio, 1, true>(x, w, sig, yR[0], yfn);
   }
@@ -400,7 +424,7 @@ __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, 
 #pragma unroll
       for (int r = 0; r < B; ++r) yfm[r] = yL[NR - 1][r];
     } else {
-      ldlv<B, S, Tio, 1, true>(x.yin, (f - 1) * B, yfm);
+      ld_yfwd<B, S, Tio>(x, f - 1, yfm);
     }
     spow<B, S>(S(sS[-1]), w.s2, am);
     stl<S, Tio, 1, true>(x.gs, 1, f - 1, lds<B, S>(am, yL[0], yfm, yn[0], yfn));

@@ -125,6 +125,10 @@ struct Grp {
   Str<Tio, P> c, d, s, yin, gy, yout, gc, gd, gs;
   const Tio* u[P];
   Tio* gu[P];
+  // pipeline P2 only (smnn_chunk.cuh): y's fp32 remainder written (forward) / read (backward)
+  // in shared memory at element offset ylo_off (relative to time index 0: may be negative)
+  bool ylo_out = false, ylo_in = false;
+  int ylo_off = 0;
   bool gu_on;
   int nv, T, n_iv;
   template <int B>

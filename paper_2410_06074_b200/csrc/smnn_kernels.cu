@@ -441,6 +441,14 @@ int kernel_path(const smnn_problem* p, bool bwd);
 // dl/dbeta (two right-hand sides, one factorisation); the other paths run the backward as SMNN_F64 on promoted copies instead: inputs and
 // dl/dy widened to fp64 in the workspace, the fp64 forward (y in fp64), the
 // fp64 backward, gradients narrowed into the caller's fp32 outputs.
+// SMNN_F32_C64 on the pipeline in both directions: the forward can hand the
+// backward the fp32 remainder y_lo of its fp64 y (smnn_factor_solve_fwd_ex), so
+// the backward reads y_hi + y_lo instead of re-solving y (one right-hand side).
+bool ylo_used(const smnn_problem* p) {
+  return p->dtype == SMNN_F32_C64 && kernel_path(p, false) == SMNN_PATH_PIPE &&
+         kernel_path(p, true) == SMNN_PATH_PIPE && smnn::pipe_ylo_eligible(p);
+}
+
 bool promote_bwd(const smnn_problem* p) {
   if (p->dtype != SMNN_F32_C64) return false;
   const int path = kernel_path(p, true);
@@ -786,6 +794,7 @@ struct smnn_plan {
   smnn_problem p;
   void* buf = nullptr;   // one allocation
   void *c, *d, *u, *s, *gy, *y, *gc, *gd, *gu, *gs, *ws;
+  void* ylo = nullptr;  // SMNN_F32_C64: fp32 remainder of y, forward -> backward (smnn_solve_bwd_ex)
   int32_t* info;     // backward pass
   int32_t* info_f;   // forward pass (merged into info: the first breakdown wins)
   size_t ws_bytes = 0;
@@ -843,9 +852,21 @@ int smnn_assemble(const smnn_problem* p, const void* coeffs, const void* rhs, co
   return dispatch_assemble<float, double>(p, a, (float*)M_diag, (float*)N_sub, (float*)beta, st);
 }
 
+int smnn_ylo_used(const smnn_problem* p) {
+  int e;
+  if ((e = validate(p))) return e;
+  return ylo_used(p) ? 1 : 0;
+}
+
 int smnn_factor_solve_fwd(const smnn_problem* p, const void* coeffs, const void* rhs, const void* iv,
                           const void* steps, void* y, int32_t* info, void* workspace, size_t workspace_bytes_,
                           void* stream) {
+  return smnn_factor_solve_fwd_ex(p, coeffs, rhs, iv, steps, y, nullptr, info, workspace, workspace_bytes_, stream);
+}
+
+int smnn_factor_solve_fwd_ex(const smnn_problem* p, const void* coeffs, const void* rhs, const void* iv,
+                             const void* steps, void* y, void* y_lo, int32_t* info, void* workspace,
+                             size_t workspace_bytes_, void* stream) {
   int e;
   if ((e = validate(p)) || (e = need(coeffs, "coeffs")) || (e = need(rhs, "rhs")) || (e = need(iv, "iv")) ||
       (e = need_steps(p, steps)) || (e = need(y, "y")))
@@ -866,12 +887,26 @@ int smnn_factor_solve_fwd(const smnn_problem* p, const void* coeffs, const void*
   set_inputs(a, coeffs, rhs, iv, steps);
   a.y_out = (float*)y; a.info = info; a.ckpt = workspace;
   if (p->dtype == SMNN_F32) return dispatch_fused<float, float, false>(p, a, st);
+  if (y_lo && !ylo_used(p)) {  // not this path's: y_lo = 0 (y_hi + y_lo = y_hi stays a valid pair)
+    const size_t nb = size_t(p->n_inst) * size_t(p->T) * size_t(p->order + 1) * sizeof(float);
+    if ((e = check_cuda(cudaMemsetAsync(y_lo, 0, nb, st), "y_lo clear"))) return e;
+  } else {
+    a.y_lo_out = static_cast<float*>(y_lo);
+  }
   return dispatch_fused<float, double, false>(p, a, st);
 }
 
 int smnn_solve_bwd(const smnn_problem* p, const void* coeffs, const void* rhs, const void* iv, const void* steps,
                    const void* y, const void* grad_y, void* grad_coeffs, void* grad_rhs, void* grad_iv,
                    void* grad_steps, int32_t* info, void* workspace, size_t workspace_bytes_, void* stream) {
+  return smnn_solve_bwd_ex(p, coeffs, rhs, iv, steps, y, nullptr, grad_y, grad_coeffs, grad_rhs, grad_iv, grad_steps,
+                           info, workspace, workspace_bytes_, stream);
+}
+
+int smnn_solve_bwd_ex(const smnn_problem* p, const void* coeffs, const void* rhs, const void* iv, const void* steps,
+                      const void* y, const void* y_lo, const void* grad_y, void* grad_coeffs, void* grad_rhs,
+                      void* grad_iv, void* grad_steps, int32_t* info, void* workspace, size_t workspace_bytes_,
+                      void* stream) {
   int e;
   if ((e = validate(p)) || (e = need(coeffs, "coeffs")) || (e = need(rhs, "rhs")) || (e = need(iv, "iv")) ||
       (e = need_steps(p, steps)) || (e = need(y, "y")) || (e = need(grad_y, "grad_y")))
@@ -889,6 +924,22 @@ int smnn_solve_bwd(const smnn_problem* p, const void* coeffs, const void* rhs, c
     a.g_coeffs = (double*)grad_coeffs; a.g_rhs = (double*)grad_rhs; a.g_iv = (double*)grad_iv;
     a.g_steps = p->T > 1 ? (double*)grad_steps : nullptr; a.info = info; a.ckpt = workspace;
     return dispatch_fused<double, double, true>(p, a, st);
+  }
+  if (y_lo && ylo_used(p)) {  // one right-hand side: y = y_hi + y_lo read, not re-solved
+    auto a = make_args<float>(p);
+    set_inputs(a, coeffs, rhs, iv, steps);
+    a.y_in = (const float*)y; a.y_lo_in = (const float*)y_lo; a.grad_y = (const float*)grad_y;
+    a.g_coeffs = (float*)grad_coeffs; a.g_rhs = (float*)grad_rhs; a.g_iv = (float*)grad_iv;
+    a.g_steps = p->T > 1 ? (float*)grad_steps : nullptr; a.info = info; a.ckpt = workspace;
+    return dispatch_fused<float, double, true>(p, a, st);
+  }
+  if (y_lo && ylo_used(p)) {  // one right-hand side: y = y_hi + y_lo read, not re-solved
+    auto a = make_args<float>(p);
+    set_inputs(a, coeffs, rhs, iv, steps);
+    a.y_in = (const float*)y; a.y_lo_in = (const float*)y_lo; a.grad_y = (const float*)grad_y;
+    a.g_coeffs = (float*)grad_coeffs; a.g_rhs = (float*)grad_rhs; a.g_iv = (float*)grad_iv;
+    a.g_steps = p->T > 1 ? (float*)grad_steps : nullptr; a.info = info; a.ckpt = workspace;
+    return dispatch_fused<float, double, true>(p, a, st);
   }
   if (promote_bwd(p))
     return bwd_promoted(p, coeffs, rhs, iv, steps, grad_y, grad_coeffs, grad_rhs, grad_iv, grad_steps, info, workspace,
@@ -949,11 +1000,13 @@ int smnn_plan_create(smnn_plan** plan, const smnn_problem* p) {
   const size_t sz_c = al(n * T * b * es), sz_d = al(n * T * es), sz_u = al(n * p->n_iv * es),
                sz_s = al(n * std::max<size_t>(T - 1, 1) * es), sz_info = al(n * 4);
   q->ws_bytes = al(workspace_bytes(p));
-  const size_t total = 4 * sz_c + 2 * sz_d + 2 * sz_u + 2 * sz_s + 2 * sz_info + q->ws_bytes;
+  const bool c64 = p->dtype == SMNN_F32_C64;
+  const size_t total = (c64 ? 5 : 4) * sz_c + 2 * sz_d + 2 * sz_u + 2 * sz_s + 2 * sz_info + q->ws_bytes;
   if ((e = check_cuda(cudaMalloc(&q->buf, total), "cudaMalloc(plan)"))) { delete q; return e; }
   char* ptr = static_cast<char*>(q->buf);
   auto take = [&](size_t s) { void* r = ptr; ptr += s; return r; };
   q->c = take(sz_c); q->gy = take(sz_c); q->y = take(sz_c); q->gc = take(sz_c);
+  if (c64) q->ylo = take(sz_c);
   q->d = take(sz_d); q->gd = take(sz_d);
   q->u = take(sz_u); q->gu = take(sz_u);
   q->s = take(sz_s); q->gs = take(sz_s);
@@ -1043,10 +1096,11 @@ int smnn_plan_fwd_bwd_host(smnn_plan* q, const void* coeffs, const void* rhs, co
       return e;
     smnn_problem pg = *p;
     pg.n_inst = ni;
-    if ((e = smnn_factor_solve_fwd(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc),
-                                   q->info_f + i0, q->ws, q->ws_bytes, q->scomp)))
+    void* ylo = q->ylo ? D(q->ylo, oc) : nullptr;
+    if ((e = smnn_factor_solve_fwd_ex(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc), ylo,
+                                      q->info_f + i0, q->ws, q->ws_bytes, q->scomp)))
       return e;
-    if ((e = smnn_solve_bwd(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc), D(q->gy, oc),
+    if ((e = smnn_solve_bwd_ex(&pg, D(q->c, oc), D(q->d, od), D(q->u, ou), D(q->s, os), D(q->y, oc), ylo, D(q->gy, oc),
                             D(q->gc, oc), D(q->gd, od), D(q->gu, ou), D(q->gs, os),
                             q->info + i0, q->ws, q->ws_bytes, q->scomp)))
       return e;

@@ -47,12 +47,17 @@ struct PipePlan {
 
 // Right-hand sides of a pipeline call: 2 in the SMNN_F32_C64 backward (dl/dy and
 // beta: y is re-solved in fp64 beside lambda; see include/smnn.h smnn_solve_bwd).
-int pipe_nr(const smnn_problem* p, bool bwd) { return (bwd && p->dtype == SMNN_F32_C64) ? 2 : 1; }
+// With the forward's fp32 remainder of y (ylo: Args::y_lo_in) the backward reads
+// y_hi + y_lo and needs one right-hand side.
+int pipe_nr(const smnn_problem* p, bool bwd, bool ylo) {
+  return (bwd && p->dtype == SMNN_F32_C64 && !ylo) ? 2 : 1;
+}
 
 template <int B, class S>
-PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
+PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd, bool ylo) {
   PipePlan q;
-  const int nr = pipe_nr(p, bwd);
+  const int nr = pipe_nr(p, bwd, ylo);
+  const bool c64 = sizeof(S) > es;
   constexpr int CM = PipeCM<B, S>::value;
   const int T = p->T;
   if (p->threads_per_inst != 0 || T < 4) return q;
@@ -104,18 +109,20 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
     L.off_s = take(size_t(steps) * es + 32);
     L.off_g = bwd ? take(size_t(steps) * B * es + 32) : 0;
     L.off_y = (bwd && p2 && nr == 1) ? take(size_t(steps) * B * es + 32) : 0;
+    // SMNN_F32_C64: y's fp32 remainder, forward out / backward (one right-hand side) in
+    L.off_yl = (c64 && p2 && (!bwd || nr == 1)) ? take(size_t(steps) * B * es + 32) : 0;
     L.off_h = p2 ? 0 : take(size_t(PSep<B>::LT + nr * B) * SMNN_PIPE_NT * ls);
     L.off_bar = take(16);
     return off;
   };
   // chunk-kernel CTA: 128 chunks, fewer when its staged range would exceed
-  // 64 KB (fp64 storage with long chunks: keep >= 3 CTAs per SM; measured
-  // 1 CTA/SM and 5x slower at order 1, T = 1e4, f64 before)
+  // 72 KB (fp64 storage with long chunks: keep >= 3 CTAs per SM; measured
+  // 1 CTA/SM and 5x slower at order 1, T = 1e4, f64 before; 3 x 72 KB fit)
   for (;;) {
     steps = q.NT * CM + 2;  // points of one CTA range (+ s_{ta-1}, y_{ta-1})
     q.smem_p1 = layout(q.L1, false);
     q.smem_p2 = layout(q.L2, true);
-    if (q.NT <= 32 || std::max(q.smem_p1, q.smem_p2) <= 64 * 1024) break;
+    if (q.NT <= 32 || std::max(q.smem_p1, q.smem_p2) <= 72 * 1024) break;
     q.NT /= 2;
   }
   q.parts = (K + q.NT - 1) / q.NT;
@@ -148,24 +155,24 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd) {
 }
 
 template <class S>
-PipePlan plan_S(const smnn_problem* p, size_t es, bool bwd) {
+PipePlan plan_S(const smnn_problem* p, size_t es, bool bwd, bool ylo) {
   switch (p->order) {
-    case 0: return plan_B<1, S>(p, es, bwd);
-    case 1: return plan_B<2, S>(p, es, bwd);
-    case 2: return plan_B<3, S>(p, es, bwd);
-    default: return plan_B<4, S>(p, es, bwd);
+    case 0: return plan_B<1, S>(p, es, bwd, ylo);
+    case 1: return plan_B<2, S>(p, es, bwd, ylo);
+    case 2: return plan_B<3, S>(p, es, bwd, ylo);
+    default: return plan_B<4, S>(p, es, bwd, ylo);
   }
 }
 
-PipePlan plan_of(const smnn_problem* p, bool bwd) {
-  if (p->dtype == SMNN_F32) return plan_S<float>(p, 4, bwd);
-  return plan_S<double>(p, p->dtype == SMNN_F64 ? 8 : 4, bwd);
+PipePlan plan_of(const smnn_problem* p, bool bwd, bool ylo = false) {
+  if (p->dtype == SMNN_F32) return plan_S<float>(p, 4, bwd, false);
+  return plan_S<double>(p, p->dtype == SMNN_F64 ? 8 : 4, bwd, ylo && p->dtype == SMNN_F32_C64);
 }
 
 template <int B, class Tio, class S, bool BWD, int NR>
 int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
   constexpr int CM = PipeCM<B, S>::value;
-  PipePlan q = plan_B<B, S>(p, sizeof(Tio), BWD);
+  PipePlan q = plan_B<B, S>(p, sizeof(Tio), BWD, BWD && NR == 1 && sizeof(S) > sizeof(Tio));
   if (!q.ok) return 0;
   auto k1 = pipe_p1_kernel<B, Tio, S, BWD, CM, NR>;
   auto k2 = pipe_sep_kernel<B, S, NR>;
@@ -200,7 +207,7 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
   auto chain = [&](cudaStream_t s) {
     PipeL L1 = level(0), L2 = level(0);
     L2.off_c = q.L2.off_c; L2.off_d = q.L2.off_d; L2.off_s = q.L2.off_s; L2.off_g = q.L2.off_g;
-    L2.off_y = q.L2.off_y; L2.off_h = q.L2.off_h; L2.off_bar = q.L2.off_bar;
+    L2.off_y = q.L2.off_y; L2.off_h = q.L2.off_h; L2.off_bar = q.L2.off_bar; L2.off_yl = q.L2.off_yl;
     k1<<<unsigned(n * q.parts), q.NT, q.smem_p1, s>>>(a, L1);
     for (int l = 0; l < q.levels; ++l)
       pipe_sepl_kernel<B, S, NR><<<unsigned(n * (q.Kl[l] / (kSepLM * kSepLNT))), kSepLNT, 0, s>>>(level(l), level(l + 1),
@@ -238,7 +245,8 @@ int launch_order_nr(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, 
 
 template <class Tio, class S, bool BWD>
 int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::string& err) {
-  if constexpr (BWD && sizeof(S) > sizeof(Tio)) {  // SMNN_F32_C64 backward: y re-solved
+  if constexpr (BWD && sizeof(S) > sizeof(Tio)) {  // SMNN_F32_C64 backward: y_hi + y_lo read, or re-solved
+    if (a.y_lo_in) return launch_order_nr<Tio, S, BWD, 1>(p, a, st, err);
     return launch_order_nr<Tio, S, BWD, 2>(p, a, st, err);
   } else {
     return launch_order_nr<Tio, S, BWD, 1>(p, a, st, err);
@@ -248,6 +256,12 @@ int launch_order(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std
 }  // namespace
 
 bool pipe_eligible(const smnn_problem* p, bool bwd) { return plan_of(p, bwd).ok; }
+
+bool pipe_ylo_eligible(const smnn_problem* p) {
+  if (p->dtype != SMNN_F32_C64) return false;
+  const PipePlan f = plan_of(p, false), b = plan_of(p, true), r = plan_of(p, true, true);
+  return f.ok && r.ok && b.ok && r.NT == b.NT;  // not where staging y_lo would shrink the CTAs
+}
 
 int pipe_launches(const smnn_problem* p, bool bwd) {
   const PipePlan q = plan_of(p, bwd);
@@ -259,6 +273,7 @@ size_t pipe_workspace_bytes(const smnn_problem* p) {
   size_t n = 0;
   if (f.ok) n = std::max(n, f.ws_total);
   if (b.ok) n = std::max(n, b.ws_total);
+  if (const PipePlan r = plan_of(p, true, true); r.ok) n = std::max(n, r.ws_total);
   return n;
 }
 

@@ -24,8 +24,10 @@
 // bytes per field:
 //   sep1 [g][PSep<B,NR>::N][K]  D_own (lower, packed), R_own, A_rl, A_ll (packed), r_l
 //   ysep [g][NR B][K]           y at the separators (per right-hand side)
-// NR = 2 in the SMNN_F32_C64 backward: dl/dy and beta share the factorisation,
-// so y is re-solved in fp64 beside lambda instead of read from fp32 storage.
+// NR = 2 in the SMNN_F32_C64 backward without the forward's y remainder: dl/dy
+// and beta share the factorisation, so y is re-solved in fp64 beside lambda
+// instead of read from fp32 storage.  With the remainder (Args::y_lo_in) the
+// backward is NR = 1 and reads y_hi + y_lo (smnn_solve_bwd_ex).
 //   cfail[g][K]              1 + first point of a chunk whose pivots broke down, else INT_MAX
 #pragma once
 
@@ -74,6 +76,7 @@ struct PipeL {
   int NT;         // threads per CTA of the chunk kernels
   int parts;      // CTAs per instance of the chunk kernels
   int off_c, off_d, off_s, off_g, off_y, off_h, off_bar;  // shared-memory byte offsets (16-aligned)
+  int off_yl;     // P2, SMNN_F32_C64: y's fp32 remainder (forward out / backward in), 0 = none
   void* sep1;
   void* ysep;
   int* cfail;
@@ -628,14 +631,20 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? (NR == 2
   const Span<Tio> ps(a.steps + tsb + R.slo, R.shi - R.slo);
   const Span<Tio> pg(BWD ? a.grad_y + tb + R.ta * B : a.coeffs, BWD ? (R.tb - R.ta) * B : 0);
   const Span<Tio> py(YIN ? a.y_in + tb + ylo * B : a.coeffs, YIN ? (R.tb - ylo) * B : 0);
+  // SMNN_F32_C64 y remainder: staged in (backward) or stored out (forward) through its own region
+  constexpr bool C64 = sizeof(S) > sizeof(Tio);
+  const bool yl_in = C64 && YIN && a.y_lo_in && L.off_yl, yl_out = C64 && !BWD && a.y_lo_out && L.off_yl;
+  const Span<Tio> pyl(yl_in ? a.y_lo_in + tb + ylo * B : a.coeffs, yl_in ? (R.tb - ylo) * B : 0);
+  const Span<Tio> pyo(yl_out ? a.y_lo_out + tb + R.ta * B : a.coeffs, yl_out ? (R.tb - R.ta) * B : 0);
   if (tid == 0) {
     mbar_init(bar, 1);
-    mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes);
+    mbar_expect_tx(bar, pc.bytes + pd.bytes + ps.bytes + pg.bytes + py.bytes + pyl.bytes);
     bulk_g2s(sm + L.off_c, pc.lo, pc.bytes, bar);
     bulk_g2s(sm + L.off_d, pd.lo, pd.bytes, bar);
     if (ps.bytes) bulk_g2s(sm + L.off_s, ps.lo, ps.bytes, bar);
     if (BWD) bulk_g2s(sm + L.off_g, pg.lo, pg.bytes, bar);
     if (YIN) bulk_g2s(sm + L.off_y, py.lo, py.bytes, bar);
+    if (pyl.bytes) bulk_g2s(sm + L.off_yl, pyl.lo, pyl.bytes, bar);
   }
   constexpr int E = int(sizeof(Tio));
   const int k = R.c0 + tid;
@@ -653,6 +662,10 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? (NR == 2
   x.yout.o[0] = oc; x.gc.o[0] = oc; x.gd.o[0] = od; x.gs.o[0] = os;
   x.u[0] = a.iv + g * a.n_iv;
   x.gu[0] = (BWD && a.g_iv) ? a.g_iv + g * a.n_iv : nullptr;
+  const int oyl = yl_in ? L.off_yl / E + pyl.pre - ylo * B : L.off_yl / E + pyo.pre - R.ta * B;
+  x.ylo_out = yl_out;
+  x.ylo_in = yl_in;
+  x.ylo_off = oyl;
   x.c.on = x.d.on = x.s.on = true;
   x.gy.on = BWD;
   x.yin.on = YIN;
@@ -690,6 +703,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? (NR == 2
   const int nt = blockDim.x;
   if (!BWD) {
     rf_store_out(a.y_out + tb + R.ta * B, smT + oc + R.ta * B, (R.tb - R.ta) * B, tid, nt);
+    if (yl_out) rf_store_out(a.y_lo_out + tb + R.ta * B, smT + oyl + R.ta * B, (R.tb - R.ta) * B, tid, nt);
   } else {
     if (a.g_coeffs) rf_store_out(a.g_coeffs + tb + R.ta * B, smT + oc + R.ta * B, (R.tb - R.ta) * B, tid, nt);
     if (a.g_rhs) rf_store_out(a.g_rhs + t1b + R.ta, smT + od + R.ta, R.tb - R.ta, tid, nt);

@@ -45,6 +45,8 @@ struct Args {
   const Tio* y_in;     // BWD: forward solution
   const Tio* grad_y;   // BWD: dl/dy
   Tio* y_out;          // FWD: solution
+  Tio* y_lo_out;       // FWD, SMNN_F32_C64 pipeline: fp32 remainder y - (double)y_out (nullable)
+  const Tio* y_lo_in;  // BWD, SMNN_F32_C64 pipeline: that remainder (nullable: y re-solved)
   Tio* g_coeffs;       // BWD outputs (nullable)
   Tio* g_rhs;
   Tio* g_iv;
@@ -76,6 +78,7 @@ size_t pipe_workspace_bytes(const smnn_problem* p);
 // Whether rf_launch / pipe_launch would take the problem (no launch).
 bool rf_eligible(const smnn_problem* p, bool bwd);
 bool pipe_eligible(const smnn_problem* p, bool bwd);
+bool pipe_ylo_eligible(const smnn_problem* p);  // SMNN_F32_C64: forward writes / backward reads y_lo
 int pipe_launches(const smnn_problem* p, bool bwd);  // 3 + 2 per separator-hierarchy level
 
 // Cluster-resident fp64-arithmetic path (smnn_x64.cu): SMNN_F32_C64 and

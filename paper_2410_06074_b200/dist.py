@@ -77,8 +77,13 @@ def sharded_step(smnn, full: dict, grad_y: torch.Tensor, rank: int, world: int, 
     loc = {k: shard(v, rank, world) for k, v in full.items()}
     gy = shard(grad_y, rank, world)
     w = w or smnn.Weights()
-    y, info = smnn.smnn_factor_solve_fwd(loc["coeffs"], loc["rhs"], loc["iv"], loc["steps"], w, compute)
+    y_lo = None
+    if compute == "f64" and loc["coeffs"].dtype == torch.float32 and smnn.ylo_used(loc["coeffs"], loc["iv"], w, compute):
+        y, info, y_lo = smnn.smnn_factor_solve_fwd(loc["coeffs"], loc["rhs"], loc["iv"], loc["steps"], w, compute,
+                                                   with_ylo=True)
+    else:
+        y, info = smnn.smnn_factor_solve_fwd(loc["coeffs"], loc["rhs"], loc["iv"], loc["steps"], w, compute)
     loss = allreduce_loss((gy.double() * y.double()).sum(), group=group)
     y_all = gather_instances(y, n_total, group=group) if gather else None
-    g = smnn.smnn_solve_bwd(loc["coeffs"], loc["rhs"], loc["iv"], loc["steps"], y, gy, w, compute)
+    g = smnn.smnn_solve_bwd(loc["coeffs"], loc["rhs"], loc["iv"], loc["steps"], y, gy, w, compute, y_lo=y_lo)
     return y_all, loss, g

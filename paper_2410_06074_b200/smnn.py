@@ -21,7 +21,7 @@ from . import _abi
 
 __all__ = [
     "Weights", "smnn_assemble", "smnn_factor_solve_fwd", "smnn_solve_bwd", "smnn_factor",
-    "smnn_substitute", "SMNNSolve", "smnn_solve", "workspace_bytes", "HostPlan", "kernel_path",
+    "smnn_substitute", "SMNNSolve", "smnn_solve", "workspace_bytes", "HostPlan", "kernel_path", "ylo_used",
 ]
 
 
@@ -129,29 +129,48 @@ def smnn_assemble(coeffs, rhs, iv, steps, w: Weights = Weights(), compute=None):
     return M, N, beta
 
 
+def ylo_used(coeffs, iv, w: Weights = Weights(), compute=None, threads_per_inst=0, path=None) -> bool:
+    """smnn_ylo_used: does the f32c64 forward hand the backward y's fp32 remainder (include/smnn.h)?"""
+    p = _problem(coeffs, iv, w, compute, threads_per_inst, path)
+    r = _abi.load().smnn_ylo_used(ctypes.byref(p))
+    _abi.check(min(r, 0), "smnn_ylo_used")
+    return r == 1
+
+
 def smnn_factor_solve_fwd(coeffs, rhs, iv, steps, w: Weights = Weights(), compute=None, threads_per_inst=0,
-                          path=None):
+                          path=None, with_ylo=False):
     """Fused Algorithm 1: returns (y [..., T, b], info [n_inst] int32).  `path` forces a kernel path
-    ("rf" | "pipe" | "x64" | "resident" | "stream"; default automatic)."""
+    ("rf" | "pipe" | "x64" | "resident" | "stream"; default automatic).  with_ylo (float32 storage,
+    compute="f64"): also return y_lo, the fp32 remainder of the fp64 solution
+    (smnn_factor_solve_fwd_ex), as a third element, for smnn_solve_bwd(..., y_lo=y_lo)."""
     _check_inputs(coeffs, rhs, iv, steps)
     coeffs, rhs, iv, steps = map(_c, (coeffs, rhs, iv, steps))
     p = _problem(coeffs, iv, w, compute, threads_per_inst, path)
+    if with_ylo and p.dtype != _abi.SMNN_F32_C64:
+        raise ValueError("with_ylo needs float32 storage with compute='f64'")
     with torch.cuda.device(coeffs.device):
         y = torch.empty_like(coeffs)
+        y_lo = torch.empty_like(coeffs) if with_ylo else None
         info = torch.empty(p.n_inst, dtype=torch.int32, device=coeffs.device)
         ws, nws = _workspace(p, coeffs.device)
-        _abi.check(_abi.load().smnn_factor_solve_fwd(ctypes.byref(p), _ptr(coeffs), _ptr(rhs), _ptr(iv), _ptr(steps),
-                                                     _ptr(y), _ptr(info), _ptr(ws), nws, _stream(coeffs.device)),
+        _abi.check(_abi.load().smnn_factor_solve_fwd_ex(ctypes.byref(p), _ptr(coeffs), _ptr(rhs), _ptr(iv),
+                                                        _ptr(steps), _ptr(y), _ptr(y_lo), _ptr(info), _ptr(ws), nws,
+                                                        _stream(coeffs.device)),
                    "smnn_factor_solve_fwd")
-    return y, info
+    return (y, info, y_lo) if with_ylo else (y, info)
 
 
 def smnn_solve_bwd(coeffs, rhs, iv, steps, y, grad_y, w: Weights = Weights(), compute=None, threads_per_inst=0,
-                   need=(True, True, True, True), path=None):
-    """Fused Algorithm 2 + chain rule: returns (dcoeffs, drhs, div, dsteps, info)."""
+                   need=(True, True, True, True), path=None, y_lo=None):
+    """Fused Algorithm 2 + chain rule: returns (dcoeffs, drhs, div, dsteps, info).  y_lo: the forward's
+    fp32 remainder of y (smnn_factor_solve_fwd(..., with_ylo=True)); f32c64 only (smnn_solve_bwd_ex)."""
     _check_inputs(coeffs, rhs, iv, steps)
     coeffs, rhs, iv, steps, y, grad_y = map(_c, (coeffs, rhs, iv, steps, y, grad_y))
-    for name, t in (("y", y), ("grad_y", grad_y)):
+    checks = [("y", y), ("grad_y", grad_y)]
+    if y_lo is not None:
+        y_lo = _c(y_lo)
+        checks.append(("y_lo", y_lo))
+    for name, t in checks:
         if t.shape != coeffs.shape:
             raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(coeffs.shape)}")
         if t.dtype != coeffs.dtype:
@@ -159,6 +178,8 @@ def smnn_solve_bwd(coeffs, rhs, iv, steps, y, grad_y, w: Weights = Weights(), co
         if t.device != coeffs.device:
             raise ValueError(f"{name} is on {t.device}, coeffs on {coeffs.device}")
     p = _problem(coeffs, iv, w, compute, threads_per_inst, path)
+    if y_lo is not None and p.dtype != _abi.SMNN_F32_C64:
+        raise ValueError("y_lo needs float32 storage with compute='f64'")
     with torch.cuda.device(coeffs.device):
         dc = torch.empty_like(coeffs) if need[0] else None
         dd = torch.empty_like(rhs) if need[1] else None
@@ -166,9 +187,9 @@ def smnn_solve_bwd(coeffs, rhs, iv, steps, y, grad_y, w: Weights = Weights(), co
         ds = torch.empty_like(steps) if need[3] and steps.numel() else None
         info = torch.empty(p.n_inst, dtype=torch.int32, device=coeffs.device)
         ws, nws = _workspace(p, coeffs.device)
-        _abi.check(_abi.load().smnn_solve_bwd(ctypes.byref(p), _ptr(coeffs), _ptr(rhs), _ptr(iv), _ptr(steps),
-                                              _ptr(y), _ptr(grad_y), _ptr(dc), _ptr(dd), _ptr(du), _ptr(ds),
-                                              _ptr(info), _ptr(ws), nws, _stream(coeffs.device)),
+        _abi.check(_abi.load().smnn_solve_bwd_ex(ctypes.byref(p), _ptr(coeffs), _ptr(rhs), _ptr(iv), _ptr(steps),
+                                                 _ptr(y), _ptr(y_lo), _ptr(grad_y), _ptr(dc), _ptr(dd), _ptr(du),
+                                                 _ptr(ds), _ptr(info), _ptr(ws), nws, _stream(coeffs.device)),
                    "smnn_solve_bwd")
     if need[3] and ds is None:
         ds = torch.empty_like(steps)
@@ -217,18 +238,24 @@ class SMNNSolve(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, coeffs, rhs, iv, steps, w: Weights, compute, threads_per_inst):
-        y, info = smnn_factor_solve_fwd(coeffs, rhs, iv, steps, w, compute, threads_per_inst)
-        ctx.save_for_backward(coeffs, rhs, iv, steps, y)
+        lo = (coeffs.dtype == torch.float32 and compute == "f64"
+              and ylo_used(coeffs, iv, w, compute, threads_per_inst))
+        if lo:  # f32c64 on the pipeline: keep y's fp32 remainder for the backward
+            y, info, y_lo = smnn_factor_solve_fwd(coeffs, rhs, iv, steps, w, compute, threads_per_inst, with_ylo=True)
+        else:
+            (y, info), y_lo = smnn_factor_solve_fwd(coeffs, rhs, iv, steps, w, compute, threads_per_inst), None
+        ctx.save_for_backward(coeffs, rhs, iv, steps, y, y_lo)
         ctx.cfg = (w, compute, threads_per_inst)
         ctx.mark_non_differentiable(info)
         return y, info
 
     @staticmethod
     def backward(ctx, grad_y, _ginfo):
-        coeffs, rhs, iv, steps, y = ctx.saved_tensors
+        coeffs, rhs, iv, steps, y, y_lo = ctx.saved_tensors
         w, compute, tpi = ctx.cfg
         need = ctx.needs_input_grad[:4]
-        dc, dd, du, ds, _ = smnn_solve_bwd(coeffs, rhs, iv, steps, y, grad_y.contiguous(), w, compute, tpi, need)
+        dc, dd, du, ds, _ = smnn_solve_bwd(coeffs, rhs, iv, steps, y, grad_y.contiguous(), w, compute, tpi, need,
+                                           y_lo=y_lo)
         return dc, dd, du, ds, None, None, None
 
 

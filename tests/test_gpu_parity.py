@@ -13,8 +13,11 @@ Modes (storage / arithmetic):
                            even an exact-arithmetic-minus-rounding solve loses
                            the digits), achieved logged.
   f32c64  fp32 / fp64      hard 1e-4 on y AND all four gradients, no kappa
-                           widening: the accurate fp32-storage mode the bench
-                           headlines (its backward re-solves y in fp64).
+                           widening; the backward re-solves y in fp64.
+  f32c64lo                 the same with the forward's fp32 remainder y_lo
+                           handed to the backward (smnn_*_ex; the bench's
+                           mode): backward reads y_hi + y_lo, one right-hand
+                           side; same hard 1e-4.
   f32     fp32 / fp32      the fast mode.  fp32 normal equations cannot reach
                            1e-4 at R >= 2 (R7), so: kappa-free
                            normwise backward error <= 64 u32 on y, forward
@@ -40,7 +43,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 U32 = 2.0 ** -24
 U64 = 2.0 ** -53
 GNAMES = ("dcoeffs", "drhs", "div", "dsteps")
-MODES = {"f64": (torch.float64, None), "f32c64": (torch.float32, "f64"), "f32": (torch.float32, None)}
+MODES = {"f64": (torch.float64, None), "f32c64": (torch.float32, "f64"), "f32": (torch.float32, None),
+         "f32c64lo": (torch.float32, "f64")}
 
 
 @pytest.fixture(scope="module")
@@ -149,9 +153,14 @@ def run(smnn, x, gy, mode, w=None, tpi=0, path=None):
     tdt, compute = MODES[mode]
     w = w or smnn.Weights()
     t = to_dev(x, tdt)
-    y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi, path=path)
+    y_lo = None
+    if mode == "f32c64lo":
+        y, info, y_lo = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi,
+                                                   path=path, with_ylo=True)
+    else:
+        y, info = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], w, compute, tpi, path=path)
     g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, torch.from_numpy(gy).to("cuda", tdt), w,
-                            compute, tpi, path=path)
+                            compute, tpi, path=path, y_lo=y_lo)
     torch.cuda.synchronize()
     assert int(info.abs().max()) == 0 and int(g[4].abs().max()) == 0
     assert torch.isfinite(y).all() and all(torch.isfinite(z).all() for z in g[:4])
@@ -185,7 +194,7 @@ def test_assemble_f64(smnn, n, T, R, n_iv, tpi):
 
 
 @pytest.mark.parametrize("n,T,R,n_iv,tpi", CASES)
-@pytest.mark.parametrize("mode", ["f64", "f32c64", "f32"])
+@pytest.mark.parametrize("mode", ["f64", "f32c64", "f32c64lo", "f32"])
 def test_fused_fwd_bwd(smnn, mode, n, T, R, n_iv, tpi):
     x = inputs_in(make_inputs(n, T, R, n_iv, dtype="f64", seed=10 * T + R), mode)
     gy = make_grad_y(n, T, R, dtype="f64" if mode == "f64" else "f32", seed=T)
@@ -193,7 +202,7 @@ def test_fused_fwd_bwd(smnn, mode, n, T, R, n_iv, tpi):
     y, g = run(smnn, x, gy, mode, smnn.Weights(*W), tpi)
     e = errors(y, g, y_ref, g_ref)
     rec = dict(mode=mode, n=n, T=T, R=R, n_iv=n_iv, tpi=tpi, err=e)
-    if mode == "f32c64":
+    if mode.startswith("f32c64"):
         log("fused_fwd_bwd", **rec)
         assert worst(e) < 1e-4, e
         return
@@ -297,8 +306,12 @@ def test_host_plan_matches_device(smnn, n, T, dt):
     plan.fwd_bwd(h["coeffs"], h["rhs"], h["iv"], h["steps"], hg, *out, info=info)
     torch.cuda.synchronize()
     t = to_dev(x, torch.float32)
-    y, _ = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute)
-    g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, hg.cuda(), compute=compute)
+    if compute == "f64":  # the plan hands the forward's y remainder to the backward (smnn_*_ex)
+        y, _, y_lo = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute,
+                                                with_ylo=True)
+    else:
+        (y, _), y_lo = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute), None
+    g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, hg.cuda(), compute=compute, y_lo=y_lo)
     assert torch.equal(out[0], y.cpu())
     for a, b in zip(out[1:], g[:4]):
         assert torch.equal(a, b.cpu())
@@ -333,7 +346,7 @@ PATH_CASES = [  # (n, T, R, n_iv): every kernel path must match the oracle, forc
 
 @pytest.mark.parametrize("path", ["rf", "pipe", "x64", "resident", "stream"])
 @pytest.mark.parametrize("n,T,R,n_iv", PATH_CASES)
-@pytest.mark.parametrize("mode", ["f64", "f32c64", "f32"])
+@pytest.mark.parametrize("mode", ["f64", "f32c64", "f32c64lo", "f32"])
 def test_forced_kernel_paths(smnn, path, n, T, R, n_iv, mode):
     """Every kernel path (including the ones "auto" does not pick for a shape),
     forced through smnn_problem.path, against the oracle: y and all gradients.
@@ -349,7 +362,7 @@ def test_forced_kernel_paths(smnn, path, n, T, R, n_iv, mode):
     y, g = run(smnn, x, gy, mode, smnn.Weights(*W), path=path)
     e = errors(y, g, y_ref, g_ref)
     rec = dict(path=path, ran=got, mode=mode, n=n, T=T, R=R, err=e)
-    if mode == "f32c64":
+    if mode.startswith("f32c64"):
         log("forced_kernel_paths", **rec)
         assert max(e["y"]) < 1e-4, e
         assert worst(e) < 1e-4, e  # every fp64-arithmetic backward re-solves y in fp64
@@ -385,10 +398,10 @@ def test_full_size_benched_mode(smnn, name):
     k = FULL[name]
     idx = np.arange(wl.n_inst) if k is None else np.linspace(0, wl.n_inst - 1, k).astype(int)
     y_ref, g_ref = oracle_refs(x, gy, idx)
-    y, g = run(smnn, x, gy, "f32c64")
+    y, g = run(smnn, x, gy, "f32c64lo")
     e = errors(y[idx], [z[idx] for z in g], y_ref, g_ref)
     paths = [smnn.kernel_path(wl.n_inst, wl.T, wl.order, wl.n_iv, torch.float32, "f64", bwd=b) for b in (0, 1)]
-    log("full_size_benched_mode", workload=name, checked=len(idx), paths=paths, err=e)
+    log("full_size_benched_mode", workload=name, mode="f32c64lo", checked=len(idx), paths=paths, err=e)
     assert worst(e) < 1e-4, e
 
 
@@ -417,7 +430,7 @@ CORNERS = {  # configs[4] scaling-sweep corners: workload -> instances checked a
 }
 
 
-@pytest.mark.parametrize("mode", ["f32c64", "f64"])  # the top decorator varies fastest: one input set per name
+@pytest.mark.parametrize("mode", ["f32c64lo", "f64"])  # the top decorator varies fastest: one input set per name
 @pytest.mark.parametrize("name", list(CORNERS))
 def test_scaling_sweep_corners(smnn, name, mode):
     """BASELINE.json configs[4] corners (T = 1e2 .. 1e6, B*D up to 65536, order 2 and
@@ -443,10 +456,38 @@ def test_scaling_sweep_corners(smnn, name, mode):
         sub = {k: v[idx[:1]] for k, v in x.items()}
         rec["kappa"] = kappa(sub, 0, (1.0, 1.0, 1.0))
     log("scaling_sweep_corners", **rec)
-    if mode == "f32c64":
+    if mode == "f32c64lo":
         assert worst(e) < 1e-4, e
     elif wl.order <= 2:
         assert max(e["y"]) < 1e-9 and worst(e) < 4e-9, e
     else:
         tol = max(1e-9, 16 * rec["kappa"] * U64)
         assert max(e["y"]) < tol and worst(e) < 4 * tol, (e, rec["kappa"])
+
+
+@pytest.mark.parametrize("n,T,R,n_iv", [(3, 64, 2, 2), (2, 1000, 2, 2), (2, 777, 1, 1), (2, 1461, 2, 2),
+                                        (2, 257, 3, 4), (2, 30000, 2, 2), (2, 3, 2, 2)])
+def test_ylo_carries_fp64_solution(smnn, n, T, R, n_iv):
+    """smnn_factor_solve_fwd_ex (f32c64): y_lo is the fp32 remainder of the fp64
+    solution, so (double)y + (double)y_lo matches the fp64 oracle far below fp32
+    rounding (orders <= 2: 1e-9, order 3: its kappa bound), y itself is that
+    solution rounded to fp32 (|y_lo| <= ulp(y) / 2), and where smnn_ylo_used is
+    0 (shapes off the pipeline) y_lo is all zeros."""
+    x = inputs_in(make_inputs(n, T, R, n_iv, dtype="f64", seed=7 * T + R), "f32c64")
+    t = to_dev(x, torch.float32)
+    used = smnn.ylo_used(t["coeffs"], t["iv"], compute="f64")
+    y, info, y_lo = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute="f64",
+                                               with_ylo=True)
+    torch.cuda.synchronize()
+    assert int(info.abs().max()) == 0
+    if not used:
+        assert int(torch.count_nonzero(y_lo)) == 0
+        return
+    y_ref = O.solve_instances(x["coeffs"], x["rhs"], x["iv"], x["steps"]).numpy()
+    hi, lo = y.double().cpu().numpy(), y_lo.double().cpu().numpy()
+    ulp_half = np.abs(np.spacing(y.cpu().numpy())).astype(np.float64) / 2
+    assert (np.abs(lo) <= ulp_half * (1 + 1e-6)).all()
+    e = err_per(hi + lo, y_ref, True).max()
+    kap = max(kappa(x, i, (1.0, 1.0, 1.0)) for i in range(n)) if R == 3 else 0.0
+    log("ylo_carries_fp64_solution", n=n, T=T, R=R, kappa=kap, err={"y_hi_plus_lo": [float(e)]})
+    assert e < (1e-9 if R <= 2 else max(1e-9, 16 * kap * U64)), e
