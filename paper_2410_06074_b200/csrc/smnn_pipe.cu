@@ -69,6 +69,8 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd, bool ylo) {
     K = std::min((K + q128 - 1) / q128 * q128, T / 2);
   }
   int levels = 0, Ktop = K;
+  // (measured: a forced hierarchy level at K = 1024 -- SEPL + a 128-separator top
+  // solve + SEPR instead of sep2 -- is slower on the target, fwd 1.86 vs 1.71 ms)
   if (K > SMNN_PIPE_SEP_MAX) {  // separator hierarchy: 8 separators per thread and level
     const int64_t kmin = (int64_t(T) + CM - 1) / CM;
     for (levels = 1; levels <= kMaxLevels; ++levels) {

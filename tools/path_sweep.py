@@ -26,6 +26,7 @@ ap.add_argument("--units", type=float, default=4e7)
 ap.add_argument("--T", default="500,1000,1461,2000,3000,4000,5000,7500,10000,15000,20000")
 ap.add_argument("--paths", default="auto,x64,pipe,checkpoint")
 ap.add_argument("--lib", default=None, help="a variant build (tools/build_variant.sh)")
+ap.add_argument("--no-ylo", action="store_true", help="f32c64: backward re-solves y (no y_lo hand-off)")
 a = ap.parse_args()
 if a.lib:
     from paper_2410_06074_b200 import _abi
@@ -62,11 +63,14 @@ for T in [int(v) for v in a.T.split(",")]:
                smnn.kernel_path(n, T, R, R, tdt, compute, bwd=True, path=pth))
         if path != "auto" and path not in got:
             continue
-        y, _ = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute, path=pth)
+        lo = compute == "f64" and not a.no_ylo and smnn.ylo_used(t["coeffs"], t["iv"], compute=compute, path=pth)
+        out = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute, path=pth,
+                                         with_ylo=lo)
+        y, y_lo = out[0], (out[2] if lo else None)
         f = timeit(lambda: smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute,
-                                                      path=pth))
+                                                      path=pth, with_ylo=lo))
         b = timeit(lambda: smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, compute=compute,
-                                               path=pth))
+                                               path=pth, y_lo=y_lo))
         row[path] = {"ran": got, "fwd_ms": f, "bwd_ms": b, "fwd": n * T / f * 1e3, "bwd": n * T / b * 1e3,
                      "step": n * T / (f + b) * 1e3}
     print(json.dumps(row), flush=True)
