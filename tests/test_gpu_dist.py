@@ -60,8 +60,12 @@ def test_sharded_step_matches_single_process():
     gy = torch.from_numpy(make_grad_y(wl.n_inst, wl.T, wl.order, dtype="f32", seed=4)).cuda()
     t = {k: torch.from_numpy(v).cuda() for k, v in x.items()}
     for compute in ("f64", None):
-        y, _ = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute)
-        g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, compute=compute)
+        # the same calls sharded_step makes (f32c64: the y_lo hand-off where the pipeline takes it)
+        lo = compute == "f64" and smnn.ylo_used(t["coeffs"], t["iv"], compute=compute)
+        out = smnn.smnn_factor_solve_fwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], compute=compute, with_ylo=lo)
+        y = out[0]
+        g = smnn.smnn_solve_bwd(t["coeffs"], t["rhs"], t["iv"], t["steps"], y, gy, compute=compute,
+                                y_lo=out[2] if lo else None)
         loss = float((gy.double() * y.double()).sum())
         mine = [r for r in res if r[1] == compute]
         assert len(mine) == 2
