@@ -48,6 +48,9 @@ __device__ __forceinline__ void rcopyL(const S (&src)[B][B], S (&dst)[B][B]) {
 #ifndef SMNN_PIPE_HM4D
 #define SMNN_PIPE_HM4D 4  // fp64 arithmetic, order 3 (b = 4)
 #endif
+#ifndef SMNN_P2_SEG_RT
+#define SMNN_P2_SEG_RT 0  // 1: keep P2's run-through of the first segment for callers without P1's state
+#endif
 // P2 register segment: the factors of up to HM interior points stay in registers.
 template <int B, class S, int NR = 1>
 struct PipeHM {
@@ -105,11 +108,25 @@ __device__ __forceinline__ void lcouple_v(const S (&P)[B][B], const S (&w)[B], S
 // separator block Dsep (lower), rhs Rsep, coupling A_rl, and sum X^T X /
 // sum X^T w (to be negated into A_ll / r_l of separator k-1); true on a
 // pivot breakdown.  NR right-hand sides share the factorisation.
+//
+// seg (nullable, field stride K): a chunk P2 handles in two segments (nint >
+// HM) gets its factorisation state at point h - 1 = nint - HM - 1 stored
+// there (PSegState: L_{h-1}, w'_{h-1} with y_L = 0, and the spike sg X_{h-1},
+// so that P2 forms w'_{h-1}(y_L) = w'_{h-1}(0) - sg X_{h-1} y_L and starts the
+// second segment without re-factoring the first).
+template <int B, int NR>
+struct PSegState {
+  static constexpr int LT = B * (B + 1) / 2;
+  static constexpr int L = 0, W = LT, X = LT + NR * B, N = LT + NR * B + B * B;
+};
+
 template <int B, class Tio, class S, bool BWD, int CM, int NR = 1>
 __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u, int k, int K, int nint,
                                          const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS,
                                          S (&Dsep)[B][B], S (&Rsep)[NR][B], S (&Arl)[B][B], S (&All)[B][B],
-                                         S (&rl)[NR][B]) {
+                                         S (&rl)[NR][B], S* seg = nullptr) {
+  using SS = PSegState<B, NR>;
+  const int hcap = seg ? nint - PipeHM<B, S, NR>::value - 1 : -1;  // < 0: one segment, nothing stored
   S ap[2 * B - 1];
   if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
   S Lc[B][B], wv[NR][B], X[B][B];
@@ -198,12 +215,28 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
         }
       }
     }
+    if (i == hcap) {  // P2's state at the end of its first segment (see PSegState)
+      int e = 0;
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q <= r; ++q) seg[int64_t(SS::L + e++) * K] = Lc[r][q];
+#pragma unroll
+      for (int p = 0; p < NR; ++p)
+#pragma unroll
+        for (int r = 0; r < B; ++r) seg[int64_t(SS::W + p * B + r) * K] = wv[p][r];
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < B; ++q) seg[int64_t(SS::X + r * B + q) * K] = mul_(sg, X[r][q]);
+    }
 #pragma unroll
     for (int m = 0; m < 2 * B - 1; ++m) ap[m] = an[m];
   };
   step(0, std::true_type{});
 #pragma unroll 1
   for (int i = 1; i < nint; ++i) step(i, std::false_type{});
+
   // one pivot check per chunk: a breakdown leaves a non-finite last factor
   const bool bad = bad_(splat<S>(1.0) / Lc[B - 1][B - 1]) != 0;
   {  // Schur complement of the interior onto (sigma_{k-1}, sigma_k); ap = a(s_l)
@@ -378,7 +411,8 @@ __device__ __forceinline__ void p2_seg(const Grp<Tio, 1>& x, const Wts<S>& w, in
 template <int B, class Tio, class S, bool BWD, int CM, int NR = 1>
 __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, int k, int f, int sig, int nint,
                                          const Tio* cS, const Tio* dS, const Tio* sS, const Tio* gS,
-                                         const S (&yL)[NR][B], const S (&yR)[NR][B]) {
+                                         const S (&yL)[NR][B], const S (&yR)[NR][B], const S* seg = nullptr,
+                                         int K = 0) {
   // a chunk longer than HM is split as [0, h) + [h, nint) with the second
   // segment HM long; [0, h) is factored twice (run-through to reach the state
   // at h - 1, then stored for its back substitution).
@@ -411,7 +445,30 @@ __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, 
     // (measured: calling one stored-segment copy twice from a rolled loop
     // shrinks the code but costs more instructions than the icache saves)
     const int h = nint - HM;
-    p2_seg<B, Tio, S, BWD, HM, false, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+    if (SMNN_P2_SEG_RT == 0 || seg) {  // P1 stored the state at h - 1 (PSegState): no run-through of [0, h)
+      using SS = PSegState<B, NR>;
+      int e = 0;
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q <= r; ++q) Ls[r][q] = seg[int64_t(SS::L + e++) * K];
+      S Xs[B][B];
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < B; ++q) Xs[r][q] = seg[int64_t(SS::X + r * B + q) * K];
+#pragma unroll
+      for (int p = 0; p < NR; ++p)
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          S acc = seg[int64_t(SS::W + p * B + r) * K];
+#pragma unroll
+          for (int q = 0; q < B; ++q) acc = fnma_(Xs[r][q], yL[p][q], acc);
+          ws[p][r] = acc;
+        }
+    } else {
+      p2_seg<B, Tio, S, BWD, HM, false, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
+    }
     // (measured again with the y_lo backward: one rolled stored-segment copy called
     // twice is no faster at T = 1e4 and 8 % slower at T = 1e3 than two inlined copies)
     p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, h, HM, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);

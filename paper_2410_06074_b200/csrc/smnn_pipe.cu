@@ -42,6 +42,7 @@ struct PipePlan {
   int levels = 0;
   int Kl[kMaxLevels + 1] = {};
   size_t off_rec[kMaxLevels + 1] = {}, off_y[kMaxLevels + 1] = {}, off_fail[kMaxLevels + 1] = {};
+  size_t off_seg = 0, ws_seg = 0;  // P1 -> P2 state of two-segment chunks (level 0; 0 bytes: none)
   size_t ws_total = 0;
 };
 
@@ -141,6 +142,11 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd, bool ylo) {
     q.off_fail[l] = off;
     off += al256(size_t(p->n_inst) * q.Kl[l] * 4);
   }
+  if (CM - 1 > PipeHM<B, S>::value) {  // chunks P2 handles in two segments: P1 stores their state
+    q.off_seg = off;
+    q.ws_seg = al256(size_t(p->n_inst) * size_t(nr == 2 ? PSegState<B, 2>::N : PSegState<B, 1>::N) * K * ls);
+    off += q.ws_seg;
+  }
   q.ws_total = off;
   q.ws_sep1 = q.off_y[0];
   q.ws_ysep = q.off_fail[0] - q.off_y[0];
@@ -204,6 +210,7 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
     L.sep1 = ws + q.off_rec[l];
     L.ysep = ws + q.off_y[l];
     L.cfail = reinterpret_cast<int*>(ws + q.off_fail[l]);
+    L.seg = (l == 0 && q.ws_seg) ? ws + q.off_seg : nullptr;
     return L;
   };
   auto chain = [&](cudaStream_t s) {

@@ -80,6 +80,7 @@ struct PipeL {
   void* sep1;
   void* ysep;
   int* cfail;
+  void* seg;      // level 0, two-segment chunks: P1 -> P2 factorisation state (PSegState), else nullptr
 };
 
 // Time range of a chunk-kernel CTA: chunks [c0, c0 + nc), points [ta, tb),
@@ -107,7 +108,8 @@ __device__ __forceinline__ int sep_time(const PipeL& L, int j, int T) {
 
 // ============================================================== P1 ========
 template <int B, class Tio, class S, bool BWD, int CM, int NR>
-__global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MINB64 : 4) pipe_p1_kernel(Args<Tio> a, PipeL L) {
+__global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? ((B == 3 && NR == 1) ? 4 : SMNN_PIPE_P1_MINB64) : 4)
+    pipe_p1_kernel(Args<Tio> a, PipeL L) {  // fp64 order 2, one rhs: 4 CTAs/SM (<= 128 registers, no spills)
   using Q = PSep<B, NR>;
   unsigned char* sm = smnn_dyn_smem;
   Tio* smT = reinterpret_cast<Tio*>(sm);
@@ -145,7 +147,9 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? SMNN_PIPE_P1_MI
 
   S Dsep[B][B], Rsep[NR][B], Arl[B][B], All[B][B], rl[NR][B];
   bool bad = false;
-  if (act) bad = p1_chunk<B, Tio, S, BWD, CM, NR>(w, a.n_iv, u, k, K, nint, cS, dS, sS, gS, Dsep, Rsep, Arl, All, rl);
+  S* seg = (L.seg && act) ? reinterpret_cast<S*>(L.seg) + g * int64_t(PSegState<B, NR>::N) * K + k : nullptr;
+  if (act)
+    bad = p1_chunk<B, Tio, S, BWD, CM, NR>(w, a.n_iv, u, k, K, nint, cS, dS, sS, gS, Dsep, Rsep, Arl, All, rl, seg);
   // A_ll = -sum X^T X, r_l = -sum X^T w belong to separator k - 1: hand them to
   // the left neighbour through shared memory (the staged inputs are still in
   // use, so a region of its own); a CTA's first chunk writes them to the
@@ -696,7 +700,8 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? (NR == 2
   __syncthreads();  // barrier initialised
   mbar_wait(bar, 0);
 
-  if (act) p2_chunk<B, Tio, S, BWD, CM, NR>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR);
+  const S* seg = L.seg ? reinterpret_cast<const S*>(L.seg) + g * int64_t(PSegState<B, NR>::N) * K + k : nullptr;
+  if (act) p2_chunk<B, Tio, S, BWD, CM, NR>(x, w, k, f, sig, nint, cS, dS, sS, gS, yL, yR, seg, K);
   // ---- outputs: TMA bulk store of the aligned body, plain stores at the ends
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
