@@ -505,25 +505,25 @@ __device__ __forceinline__ void psep_ld(const S* in, int K, int NT, int j, S (&D
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q <= i; ++q) D[i][q] = in[int64_t(Q::D + e++) * K + j];
+    for (int q = 0; q <= i; ++q) D[i][q] = __ldcg(in + int64_t(Q::D + e++) * K + j);
 #pragma unroll
   for (int p = 0; p < NR; ++p)
 #pragma unroll
-    for (int i = 0; i < B; ++i) r[p][i] = in[int64_t(Q::R + p * B + i) * K + j];
+    for (int i = 0; i < B; ++i) r[p][i] = __ldcg(in + int64_t(Q::R + p * B + i) * K + j);
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
+    for (int q = 0; q < B; ++q) Bl[i][q] = __ldcg(in + int64_t(Q::BL + i * B + q) * K + j);
   if (j + 1 < K && (j + 1) % NT == 0) {
     e = 0;
 #pragma unroll
     for (int i = 0; i < B; ++i)
 #pragma unroll
-      for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], in[int64_t(Q::AL + e++) * K + j + 1]);
+      for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], __ldcg(in + int64_t(Q::AL + e++) * K + j + 1));
 #pragma unroll
     for (int p = 0; p < NR; ++p)
 #pragma unroll
-      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], in[int64_t(Q::RL + p * B + i) * K + j + 1]);
+      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], __ldcg(in + int64_t(Q::RL + p * B + i) * K + j + 1));
   }
 }
 
@@ -533,16 +533,16 @@ __device__ __forceinline__ void psep_ld_rb(const S* in, int K, int NT, int j, S 
 #pragma unroll
   for (int p = 0; p < NR; ++p)
 #pragma unroll
-    for (int i = 0; i < B; ++i) r[p][i] = in[int64_t(Q::R + p * B + i) * K + j];
+    for (int i = 0; i < B; ++i) r[p][i] = __ldcg(in + int64_t(Q::R + p * B + i) * K + j);
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
+    for (int q = 0; q < B; ++q) Bl[i][q] = __ldcg(in + int64_t(Q::BL + i * B + q) * K + j);
   if (j + 1 < K && (j + 1) % NT == 0) {
 #pragma unroll
     for (int p = 0; p < NR; ++p)
 #pragma unroll
-      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], in[int64_t(Q::RL + p * B + i) * K + j + 1]);
+      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], __ldcg(in + int64_t(Q::RL + p * B + i) * K + j + 1));
   }
 }
 template <int B, class S, int NR = 1>
@@ -551,7 +551,7 @@ __device__ __forceinline__ void psep_ld_b(const S* in, int K, int j, S (&Bl)[B][
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
+    for (int q = 0; q < B; ++q) Bl[i][q] = __ldcg(in + int64_t(Q::BL + i * B + q) * K + j);
 }
 
 }  // namespace smnn

@@ -206,15 +206,20 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? ((B == 3 && NR 
       for (int r = 0; r < B; ++r) o[int64_t(Q::RL + p * B + r) * K] = neg_(rl[p][r]);
   }
   L.cfail[g * K + k] = bad ? f + 1 : INT_MAX;  // 1 + first point of the chunk
+  // (measured: solving the separator system in each instance's last P1 CTA to
+  // finish -- atomic arrival count, sep2_body with 8 separators per thread on
+  // L2-hot records -- is slower than the separate kernel on the target:
+  // P1 + tail 1111 us vs P1 595 + SEP 456 us; the latency-bound tail holds a
+  // CTA slot ~5x longer than a chunk CTA and spills at P1's 128 registers)
 }
 
 // ============================================================== SEP =======
+// Separator system of instance g, one thread per separator (K <= 256 threads;
+// every thread of the CTA is separator k).
 template <int B, class S, int NR>
-__global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_t* info) {  // K <= 256 (larger K: sep2)
+__device__ __forceinline__ void sep1_body(const PipeL& L, int T, int32_t* info, int64_t g, int k, unsigned char* sm) {
   using BR = BRecN<B, NR>;
-  unsigned char* sm = smnn_dyn_smem;
-  const int K = L.K, k = int(threadIdx.x);
-  const int64_t g = blockIdx.x;
+  const int K = L.K;
   S* rec = reinterpret_cast<S*>(sm);
   int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * K);
   int* sfail = stime + K;
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
   } else {
     zero<B, S>(Cr);
   }
-  const int cf = L.cfail[g * K + k];
+  const int cf = __ldcg(L.cfail + g * K + k);
   __syncthreads();
   if (cf != INT_MAX) atomicMin(sfail, cf);
   rbcr2n<B, S, NR>(rec, K, k, stime, sfail, D, Bl, Cr, r);
@@ -241,6 +246,11 @@ __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_
 #pragma unroll
   for (int i = 0; i < NR * B; ++i) y[int64_t(i) * K] = rec[k * BR::N + BR::Y + i];
   if (k == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
+}
+
+template <int B, class S, int NR>
+__global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_t* info) {  // K <= 256 (larger K: sep2)
+  sep1_body<B, S, NR>(L, T, info, blockIdx.x, int(threadIdx.x), smnn_dyn_smem);
 }
 
 
@@ -439,14 +449,14 @@ __device__ __forceinline__ void sep_recover(const S* in, int K, int NTin, int j0
   }
 }
 
+// Separator system of instance g, m = K / nt separators per thread (nt threads,
+// thread t): the body of pipe_sep2_kernel.
 template <int B, class S, int MS, int NR>
-__global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
+__device__ __forceinline__ void sep2_body(const PipeL& L, int T, int32_t* info, int64_t g, int t, int nt,
+                                          unsigned char* sm) {
   using BR = BRecN<B, NR>;
-  unsigned char* sm = smnn_dyn_smem;
-  const int K = L.K, nt = blockDim.x;
-  const int t = int(threadIdx.x);
+  const int K = L.K;
   const int m = K / nt;  // separators per thread (host: K = m * nt, m <= MS)
-  const int64_t g = blockIdx.x;
   S* rec = reinterpret_cast<S*>(sm);
   int* stime = reinterpret_cast<int*>(rec + size_t(BR::N) * nt);
   int* sfail = stime + nt;
@@ -455,7 +465,7 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
   stime[t] = sep_time(L, js, T);
   const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B, NR>::N) * K;
   int cf = INT_MAX;
-  for (int j = j0; j <= js; ++j) cf = min(cf, L.cfail[g * K + j]);
+  for (int j = j0; j <= js; ++j) cf = min(cf, __ldcg(L.cfail + g * K + j));
   S Lr[MS - 1][B][B], Ds[B][B], Rs[NR][B], Bs[B][B], All[B][B], rl[NR][B];
   if (sep_local<B, S, MS, NR>(in, K, L.NT, j0, m, Lr, Ds, Rs, Bs, All, rl)) cf = min(cf, 1 + sep_time(L, j0, T));
   // hand-over (A_ll, r_l, coupling) to super-separator t - 1
@@ -507,6 +517,11 @@ __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_
   S* yo = reinterpret_cast<S*>(L.ysep) + g * int64_t(NR * B) * K;
   sep_recover<B, S, MS, NR>(in, K, L.NT, j0, m, Lr, yL, yR, yo, K);
   if (t == 0 && info) info[g] = (sfail[0] == INT_MAX) ? 0 : sfail[0];
+}
+
+template <int B, class S, int MS, int NR>
+__global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
+  sep2_body<B, S, MS, NR>(L, T, info, blockIdx.x, int(threadIdx.x), int(blockDim.x), smnn_dyn_smem);
 }
 
 // ================================================ hierarchical separators ==
