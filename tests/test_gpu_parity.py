@@ -229,7 +229,7 @@ def test_paper_step_size(smnn, R):
     x64 = make_inputs(n, T, R, R + 1, s0=0.01, dtype="f64", seed=3 + R)
     gy = make_grad_y(n, T, R, dtype="f64", seed=4)
     kap = max(kappa(x64, i, (1.0, 1.0, 1.0)) for i in range(n))
-    for mode in ("f64", "f32c64", "f32"):
+    for mode in ("f64", "f32c64", "f32c64lo", "f32"):
         x = inputs_in(x64, mode)
         y_ref, g_ref = oracle_refs(x, gy, np.arange(n), workers=1)
         y, g = run(smnn, x, gy, mode)
@@ -238,7 +238,7 @@ def test_paper_step_size(smnn, R):
         if mode == "f64":
             tol = max(1e-9, 16 * kap * U64)
             assert max(e["y"]) < tol and worst(e) < 4 * tol, (e, kap)
-        elif mode == "f32c64":
+        elif mode.startswith("f32c64"):
             assert max(e["y"]) < max(1e-4, 16 * kap * U64), (e, kap)
         else:
             for i in range(n):
