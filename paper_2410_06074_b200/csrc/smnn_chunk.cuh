@@ -126,7 +126,8 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
                                          S (&Dsep)[B][B], S (&Rsep)[NR][B], S (&Arl)[B][B], S (&All)[B][B],
                                          S (&rl)[NR][B], S* seg = nullptr) {
   using SS = PSegState<B, NR>;
-  const int hcap = seg ? nint - PipeHM<B, S, NR>::value - 1 : -1;  // < 0: one segment, nothing stored
+  constexpr bool SEG = CM - 1 > PipeHM<B, S, NR>::value;  // chunks P2 may split in two segments
+  const int hcap = (SEG && seg) ? nint - PipeHM<B, S, NR>::value - 1 : -1;  // < 0: nothing stored
   S ap[2 * B - 1];
   if (k > 0) spow<B, S>(S(sS[-1]), w.s2, ap); else zero<2 * B - 1, S>(ap);
   S Lc[B][B], wv[NR][B], X[B][B];
@@ -215,7 +216,7 @@ __device__ __forceinline__ bool p1_chunk(const Wts<S>& w, int n_iv, const Tio* u
         }
       }
     }
-    if (i == hcap) {  // P2's state at the end of its first segment (see PSegState)
+    if (SEG && i == hcap) {  // P2's state at the end of its first segment (see PSegState)
       int e = 0;
 #pragma unroll
       for (int r = 0; r < B; ++r)
@@ -505,25 +506,25 @@ __device__ __forceinline__ void psep_ld(const S* in, int K, int NT, int j, S (&D
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q <= i; ++q) D[i][q] = __ldcg(in + int64_t(Q::D + e++) * K + j);
+    for (int q = 0; q <= i; ++q) D[i][q] = in[int64_t(Q::D + e++) * K + j];
 #pragma unroll
   for (int p = 0; p < NR; ++p)
 #pragma unroll
-    for (int i = 0; i < B; ++i) r[p][i] = __ldcg(in + int64_t(Q::R + p * B + i) * K + j);
+    for (int i = 0; i < B; ++i) r[p][i] = in[int64_t(Q::R + p * B + i) * K + j];
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = __ldcg(in + int64_t(Q::BL + i * B + q) * K + j);
+    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
   if (j + 1 < K && (j + 1) % NT == 0) {
     e = 0;
 #pragma unroll
     for (int i = 0; i < B; ++i)
 #pragma unroll
-      for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], __ldcg(in + int64_t(Q::AL + e++) * K + j + 1));
+      for (int q = 0; q <= i; ++q) D[i][q] = add_(D[i][q], in[int64_t(Q::AL + e++) * K + j + 1]);
 #pragma unroll
     for (int p = 0; p < NR; ++p)
 #pragma unroll
-      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], __ldcg(in + int64_t(Q::RL + p * B + i) * K + j + 1));
+      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], in[int64_t(Q::RL + p * B + i) * K + j + 1]);
   }
 }
 
@@ -533,16 +534,16 @@ __device__ __forceinline__ void psep_ld_rb(const S* in, int K, int NT, int j, S 
 #pragma unroll
   for (int p = 0; p < NR; ++p)
 #pragma unroll
-    for (int i = 0; i < B; ++i) r[p][i] = __ldcg(in + int64_t(Q::R + p * B + i) * K + j);
+    for (int i = 0; i < B; ++i) r[p][i] = in[int64_t(Q::R + p * B + i) * K + j];
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = __ldcg(in + int64_t(Q::BL + i * B + q) * K + j);
+    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
   if (j + 1 < K && (j + 1) % NT == 0) {
 #pragma unroll
     for (int p = 0; p < NR; ++p)
 #pragma unroll
-      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], __ldcg(in + int64_t(Q::RL + p * B + i) * K + j + 1));
+      for (int i = 0; i < B; ++i) r[p][i] = add_(r[p][i], in[int64_t(Q::RL + p * B + i) * K + j + 1]);
   }
 }
 template <int B, class S, int NR = 1>
@@ -551,7 +552,7 @@ __device__ __forceinline__ void psep_ld_b(const S* in, int K, int j, S (&Bl)[B][
 #pragma unroll
   for (int i = 0; i < B; ++i)
 #pragma unroll
-    for (int q = 0; q < B; ++q) Bl[i][q] = __ldcg(in + int64_t(Q::BL + i * B + q) * K + j);
+    for (int q = 0; q < B; ++q) Bl[i][q] = in[int64_t(Q::BL + i * B + q) * K + j];
 }
 
 }  // namespace smnn

@@ -238,7 +238,7 @@ __device__ __forceinline__ void sep1_body(const PipeL& L, int T, int32_t* info, 
   } else {
     zero<B, S>(Cr);
   }
-  const int cf = __ldcg(L.cfail + g * K + k);
+  const int cf = L.cfail[g * K + k];
   __syncthreads();
   if (cf != INT_MAX) atomicMin(sfail, cf);
   rbcr2n<B, S, NR>(rec, K, k, stime, sfail, D, Bl, Cr, r);
@@ -465,7 +465,7 @@ __device__ __forceinline__ void sep2_body(const PipeL& L, int T, int32_t* info, 
   stime[t] = sep_time(L, js, T);
   const S* in = reinterpret_cast<const S*>(L.sep1) + g * int64_t(PSep<B, NR>::N) * K;
   int cf = INT_MAX;
-  for (int j = j0; j <= js; ++j) cf = min(cf, __ldcg(L.cfail + g * K + j));
+  for (int j = j0; j <= js; ++j) cf = min(cf, L.cfail[g * K + j]);
   S Lr[MS - 1][B][B], Ds[B][B], Rs[NR][B], Bs[B][B], All[B][B], rl[NR][B];
   if (sep_local<B, S, MS, NR>(in, K, L.NT, j0, m, Lr, Ds, Rs, Bs, All, rl)) cf = min(cf, 1 + sep_time(L, j0, T));
   // hand-over (A_ll, r_l, coupling) to super-separator t - 1

@@ -53,6 +53,23 @@ template <int K> __global__ void k_mix(float* out, double a, double b, float af,
   for (int k = 0; k < K; ++k) s += x[k] + y[2*k] + y[2*k+1];
   if (s == 1234.5) out[0] = (float)s;
 }
+template <int K> __global__ void k_cvt(float* out, float a) {
+  // fp32 -> fp64 -> fp32 conversions (cvt.f64.f32 / cvt.rn.f32.f64), volatile so none is folded
+  float f[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) f[k] = threadIdx.x * 1e-3f + k * a;
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double d;
+      asm volatile("cvt.f64.f32 %0, %1;" : "=d"(d) : "f"(f[k]));
+      asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(f[k]) : "d"(d));
+    }
+  float s = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) s += f[k];
+  if (s == 1234.5f) out[0] = s;
+}
 int main() {
   int dev = 0, sms, clk;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -72,6 +89,7 @@ int main() {
   run("FFMA2 (8 chains, 2 lanes)", [&] { k_ffma2<8><<<blocks, threads>>>(out, 1.0001f, 1e-7f); }, 16);
   run("DFMA (8 chains)", [&] { k_dfma<8><<<blocks, threads>>>(out, 1.0001, 1e-7); }, 8);
   run("DFMA+2 FFMA (4 chains) dfma", [&] { k_mix<4><<<blocks, threads>>>(out, 1.0001, 1e-7, 1.0001f, 1e-7f); }, 4);
+  run("F2F f32->f64->f32 (8 chains)", [&] { k_cvt<8><<<blocks, threads>>>(out, 1.0001f); }, 16);
   printf("sms %d\n", sms);
   cudaError_t e = cudaGetLastError(); printf("%s\n", cudaGetErrorString(e));
 }
