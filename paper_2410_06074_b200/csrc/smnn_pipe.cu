@@ -23,9 +23,13 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 // fp64 separator systems of SMNN_SEP2_SMALL..256 separators: sep2 with 4 per
 // thread (K / 4 threads) instead of one thread per separator -- measured on the
 // f32c64 pipeline at 4e7 instance-steps: T = 1000 8.98e9 -> 1.05e10, T = 1461
-// 7.88e9 -> 9.02e9, T = 2000 8.19e9 -> 1.04e10 instance-steps/s
+// 7.88e9 -> 9.02e9, T = 2000 8.19e9 -> 1.04e10 instance-steps/s (from K = 32,
+// T = 300: 9.98e9 -> 9.0e9, so not below 64)
 #ifndef SMNN_SEP2_SMALL
 #define SMNN_SEP2_SMALL 64
+#endif
+#ifndef SMNN_SEP2_SMALL_M  // separators per thread there (measured 2 and 8: slower at T = 1000..2000)
+#define SMNN_SEP2_SMALL_M 4
 #endif
 #ifndef SMNN_PIPE_M8_64
 #define SMNN_PIPE_M8_64 (1 << 30)
@@ -101,9 +105,9 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd, bool ylo) {
   if (q.sep2) {  // separators per thread: 4, or 8 when K/4 would exceed 256 threads
     q.m2 = (Ktop / 4 > 256 || (sizeof(S) >= 8 && Ktop >= SMNN_PIPE_M8_64)) ? 8 : 4;
     if (Ktop % (32 * q.m2) != 0 || Ktop / q.m2 > 256) q.sep2 = false;
-  } else if (sizeof(S) >= 8 && Ktop >= SMNN_SEP2_SMALL && Ktop % 4 == 0) {
+  } else if (sizeof(S) >= 8 && Ktop >= SMNN_SEP2_SMALL && Ktop % SMNN_SEP2_SMALL_M == 0) {
     q.sep2 = true;  // small K, fp64: 4 separators per thread, K / 4 threads (Lorenz, SST shapes)
-    q.m2 = 4;
+    q.m2 = SMNN_SEP2_SMALL_M;
   }
   if (Ktop > 256 && !q.sep2) return q;
   const size_t ls = sizeof(S);
