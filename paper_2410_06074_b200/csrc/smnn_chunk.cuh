@@ -471,7 +471,8 @@ __device__ __forceinline__ void p2_chunk(const Grp<Tio, 1>& x, const Wts<S>& w, 
       p2_seg<B, Tio, S, BWD, HM, false, NR>(x, w, k, f, 0, h, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
     }
     // (measured again with the y_lo backward: one rolled stored-segment copy called
-    // twice is no faster at T = 1e4 and 8 % slower at T = 1e3 than two inlined copies)
+    // twice is no faster at T = 1e4 and 8 % slower at T = 1e3 than two inlined copies;
+    // with the P1 state, one rolled copy for one or two segments spills: 5-7 % slower)
     p2_seg<B, Tio, S, BWD, HM, true, NR>(x, w, k, f, h, HM, cS, dS, sS, gS, wS, yL, Ls, ws, yn, yfn);
     zero<B, S>(Ls);
 #pragma unroll
