@@ -130,3 +130,35 @@ def test_workspace_covers_the_pipeline(lib):
                               w_gov=1, w_init=1, w_smooth=1)
         need = 4096 * K * ((2 * 6 + 2 * 3 + 9) * es + 3 * es + 4)
         assert lib.smnn_workspace_bytes(ctypes.byref(p)) >= need
+
+
+def test_ylo_hand_off_host_logic(lib):
+    """smnn_ylo_used (host logic): the f32c64 forward hands the backward y's fp32
+    remainder exactly where the pipeline serves both directions; never for
+    SMNN_F32 / SMNN_F64; the _ex entry points validate like the plain ones."""
+    import torch
+    from paper_2410_06074_b200 import _abi
+    from paper_2410_06074_b200.smnn import ylo_used
+
+    def used(n, T, R, compute="f64", dtype=torch.float32, path=None):
+        c = torch.empty(n, T, R + 1, dtype=dtype)
+        return ylo_used(c, torch.empty(n, R, dtype=dtype), compute=compute, path=path)
+
+    assert used(4096, 10000, 2)                      # north_star target: the bench's mode
+    assert used(1536, 1000, 2) and used(4096, 1461, 2)  # Lorenz, SST shapes
+    # KdV (order 3): staging y and y_lo would shrink the backward chunk CTAs
+    # (72 KB per 128 chunks exceeded), so the backward re-solves y there
+    assert not used(8192, 2000, 3)
+    assert used(64, 1000000, 2)                      # separator hierarchy
+    assert not used(4, 3, 2)                         # too short for the pipeline
+    assert not used(4, 1000, 2, path="x64")          # forced cluster path: y re-solved there
+    assert not used(4, 1000, 2, compute=None)        # fp32 arithmetic
+    assert not used(4, 1000, 2, compute=None, dtype=torch.float64)
+    p = _abi.smnn_problem(n_inst=4, T=10, order=2, n_iv=2, dtype=_abi.SMNN_F32_C64, threads_per_inst=0, path=0,
+                          w_gov=1, w_init=1, w_smooth=1)
+    assert lib.smnn_factor_solve_fwd_ex(ctypes.byref(p), None, None, None, None, None, None, None, None, 0,
+                                        None) == -1
+    assert lib.smnn_solve_bwd_ex(ctypes.byref(p), None, None, None, None, None, None, None, None, None, None,
+                                 None, None, None, 0, None) == -1
+    p.order = 7
+    assert lib.smnn_ylo_used(ctypes.byref(p)) == -3
