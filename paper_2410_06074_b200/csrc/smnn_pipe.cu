@@ -133,13 +133,13 @@ PipePlan plan_B(const smnn_problem* p, size_t es, bool bwd, bool ylo) {
     return off;
   };
   // chunk-kernel CTA: 128 chunks, fewer when its staged range would exceed
-  // 72 KB (fp64 storage with long chunks: keep >= 3 CTAs per SM; measured
-  // 1 CTA/SM and 5x slower at order 1, T = 1e4, f64 before; 3 x 72 KB fit)
+  // 75 KB (fp64 storage with long chunks: keep >= 3 CTAs per SM; measured
+  // 1 CTA/SM and 5x slower at order 1, T = 1e4, f64 before; 3 x 75 KB fit)
   for (;;) {
     steps = q.NT * CM + 2;  // points of one CTA range (+ s_{ta-1}, y_{ta-1})
     q.smem_p1 = layout(q.L1, false);
     q.smem_p2 = layout(q.L2, true);
-    if (q.NT <= 32 || std::max(q.smem_p1, q.smem_p2) <= 72 * 1024) break;
+    if (q.NT <= 32 || std::max(q.smem_p1, q.smem_p2) <= 75 * 1024) break;
     q.NT /= 2;
   }
   q.parts = (K + q.NT - 1) / q.NT;

@@ -145,10 +145,8 @@ def test_ylo_hand_off_host_logic(lib):
         return ylo_used(c, torch.empty(n, R, dtype=dtype), compute=compute, path=path)
 
     assert used(4096, 10000, 2)                      # north_star target: the bench's mode
-    assert used(1536, 1000, 2) and used(4096, 1461, 2)  # Lorenz, SST shapes
-    # KdV (order 3): staging y and y_lo would shrink the backward chunk CTAs
-    # (72 KB per 128 chunks exceeded), so the backward re-solves y there
-    assert not used(8192, 2000, 3)
+    assert used(1536, 1000, 2) and used(4096, 1461, 2) and used(8192, 2000, 3)  # Lorenz, SST, KdV shapes
+    assert not used(64, 100000, 1, dtype=torch.float32, compute=None)
     assert used(64, 1000000, 2)                      # separator hierarchy
     assert not used(4, 3, 2)                         # too short for the pipeline
     assert not used(4, 1000, 2, path="x64")          # forced cluster path: y re-solved there
