@@ -933,14 +933,6 @@ int smnn_solve_bwd_ex(const smnn_problem* p, const void* coeffs, const void* rhs
     a.g_steps = p->T > 1 ? (float*)grad_steps : nullptr; a.info = info; a.ckpt = workspace;
     return dispatch_fused<float, double, true>(p, a, st);
   }
-  if (y_lo && ylo_used(p)) {  // one right-hand side: y = y_hi + y_lo read, not re-solved
-    auto a = make_args<float>(p);
-    set_inputs(a, coeffs, rhs, iv, steps);
-    a.y_in = (const float*)y; a.y_lo_in = (const float*)y_lo; a.grad_y = (const float*)grad_y;
-    a.g_coeffs = (float*)grad_coeffs; a.g_rhs = (float*)grad_rhs; a.g_iv = (float*)grad_iv;
-    a.g_steps = p->T > 1 ? (float*)grad_steps : nullptr; a.info = info; a.ckpt = workspace;
-    return dispatch_fused<float, double, true>(p, a, st);
-  }
   if (promote_bwd(p))
     return bwd_promoted(p, coeffs, rhs, iv, steps, grad_y, grad_coeffs, grad_rhs, grad_iv, grad_steps, info, workspace,
                         workspace_bytes_, st);
