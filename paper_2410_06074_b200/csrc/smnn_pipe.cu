@@ -18,8 +18,6 @@ namespace {
 size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// fp64 separator kernel: 8 separators per thread (K/8 threads per instance,
-// up to 4 instances per SM at the same 128 registers) from this K on
 // fp64 separator systems of SMNN_SEP2_SMALL..256 separators: sep2 with 4 per
 // thread (K / 4 threads) instead of one thread per separator -- measured on the
 // f32c64 pipeline at 4e7 instance-steps: T = 1000 8.98e9 -> 1.05e10, T = 1461
@@ -31,6 +29,9 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 #ifndef SMNN_SEP2_SMALL_M  // separators per thread there (measured 2 and 8: slower at T = 1000..2000)
 #define SMNN_SEP2_SMALL_M 4
 #endif
+// fp64 separator kernel: 8 separators per thread (K/8 threads per instance,
+// up to 4 instances per SM at the same 128 registers) from this K on (off:
+// measured slower at K = 1024)
 #ifndef SMNN_PIPE_M8_64
 #define SMNN_PIPE_M8_64 (1 << 30)
 #endif
