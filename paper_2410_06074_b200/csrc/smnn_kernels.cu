@@ -790,6 +790,13 @@ static int bwd_promoted(const smnn_problem* p, const void* coeffs, const void* r
   return check_cuda(cudaGetLastError(), "narrow_kernel");
 }
 
+// most instance groups a host-plan call pipelines (<= smnn_plan::kMaxGroups);
+// measured on the f32c64 target (tools/e2e_groups.py): 8 and 16 equal (32.0 /
+// 31.7 ms per step, PCIe-bound), 32 slower (34.1 ms)
+#ifndef SMNN_PLAN_GMAX
+#define SMNN_PLAN_GMAX 8
+#endif
+
 struct smnn_plan {
   smnn_problem p;
   void* buf = nullptr;   // one allocation
@@ -1057,7 +1064,7 @@ int smnn_plan_fwd_bwd_host(smnn_plan* q, const void* coeffs, const void* rhs, co
   // one group per ~16 MiB of input, 1..8 groups (measured on B200: Lorenz,
   // 49 MB in, best at 2 groups; the 1.3 GB target best at 8)
   const size_t in_bytes = size_t(n) * T * (2 * b + 2) * es;
-  const int Gmax = int(std::max<size_t>(1, std::min<size_t>(8, in_bytes >> 24)));
+  const int Gmax = int(std::max<size_t>(1, std::min<size_t>(SMNN_PLAN_GMAX, in_bytes >> 24)));
   const int G = int(std::max<int64_t>(1, std::min<int64_t>(Gmax, n / 64)));
   auto H = [](const void* base, size_t off) { return static_cast<const char*>(base) + off; };
   auto Hm = [](void* base, size_t off) { return static_cast<char*>(base) + off; };
