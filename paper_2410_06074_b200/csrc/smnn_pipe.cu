@@ -32,6 +32,12 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 // fp64 separator kernel: 8 separators per thread (K/8 threads per instance,
 // up to 4 instances per SM at the same 128 registers) from this K on (off:
 // measured slower at K = 1024)
+// programmatic dependent launch of the separator and P2 kernels (P1 stays a full
+// stream barrier: it stages caller inputs that earlier kernels may have written).
+// Measured: +0.3..0.6 % at 4e7 instance-steps, +3..4.5 % at the Lorenz / SST sizes
+#ifndef SMNN_PIPE_PDL
+#define SMNN_PIPE_PDL 1
+#endif
 #ifndef SMNN_PIPE_M8_64
 #define SMNN_PIPE_M8_64 (1 << 30)
 #endif
@@ -237,13 +243,34 @@ int launch_B(const smnn_problem* p, const Args<Tio>& a, cudaStream_t st, std::st
       pipe_sepl_kernel<B, S, NR><<<unsigned(n * (q.Kl[l] / (kSepLM * kSepLNT))), kSepLNT, 0, s>>>(level(l), level(l + 1),
                                                                                                     T);
     const PipeL Lt = level(q.levels);
-    if (q.sep2)
-      k2b<<<unsigned(n), Lt.K / q.m2, q.smem_sep, s>>>(Lt, T, a.info);
-    else
-      k2<<<unsigned(n), Lt.K, q.smem_sep, s>>>(Lt, T, a.info);
+    // separator and P2 kernels: programmatic dependent launch (they wait for their
+    // predecessor on the device: pdl_wait in smnn_pipe.cuh)
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = SMNN_PIPE_PDL;
+    auto cfg = [&](unsigned grid, unsigned block, size_t smem) {
+      cudaLaunchConfig_t c = {};
+      c.gridDim = dim3(grid);
+      c.blockDim = dim3(block);
+      c.dynamicSmemBytes = smem;
+      c.stream = s;
+      c.attrs = pdl;
+      c.numAttrs = 1;
+      return c;
+    };
+    if (q.sep2) {
+      const cudaLaunchConfig_t c = cfg(unsigned(n), unsigned(Lt.K / q.m2), q.smem_sep);
+      cudaLaunchKernelEx(&c, k2b, Lt, T, a.info);
+    } else {
+      const cudaLaunchConfig_t c = cfg(unsigned(n), unsigned(Lt.K), q.smem_sep);
+      cudaLaunchKernelEx(&c, k2, Lt, T, a.info);
+    }
     for (int l = q.levels - 1; l >= 0; --l)
       pipe_sepr_kernel<B, S, NR><<<unsigned(n * (q.Kl[l] / (kSepLM * kSepLNT))), kSepLNT, 0, s>>>(level(l), level(l + 1));
-    k3<<<unsigned(n * q.parts), q.NT, q.smem_p2, s>>>(a, L2);
+    {
+      const cudaLaunchConfig_t c = cfg(unsigned(n * q.parts), unsigned(q.NT), q.smem_p2);
+      cudaLaunchKernelEx(&c, k3, a, L2);
+    }
   };
   // (measured: splitting the instances into 2 groups on separate streams, so
   // one group's separator kernel overlaps the other's chunk kernels, gave no

@@ -69,6 +69,14 @@ namespace smnn {
 #define SMNN_PIPE_SEP_MAX 2048
 #endif
 
+// Programmatic dependent launch (sm_90+): the separator and P2 kernels are
+// launched with programmatic stream serialisation (smnn_pipe.cu), so they may
+// start while the previous kernel drains; griddepcontrol.wait blocks until the
+// previous grid has completed and its memory is visible (a no-op when the
+// kernel was launched normally), launch_dependents lets the next one start.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct PipeL {
   int K;          // chunks (= separators) per instance (at this level of the separator hierarchy)
   int K0;         // level-0 separators (time mapping for `info`)
@@ -250,6 +258,8 @@ __device__ __forceinline__ void sep1_body(const PipeL& L, int T, int32_t* info, 
 
 template <int B, class S, int NR>
 __global__ void __launch_bounds__(256, 2) pipe_sep_kernel(PipeL L, int T, int32_t* info) {  // K <= 256 (larger K: sep2)
+  pdl_trigger();  // P2 may launch (and stage its inputs) while this grid drains
+  pdl_wait();     // P1's records complete and visible
   sep1_body<B, S, NR>(L, T, info, blockIdx.x, int(threadIdx.x), smnn_dyn_smem);
 }
 
@@ -526,6 +536,8 @@ __device__ __forceinline__ void sep2_body(const PipeL& L, int T, int32_t* info, 
 
 template <int B, class S, int MS, int NR>
 __global__ void __launch_bounds__(256, sizeof(S) >= 8 ? SMNN_SEP2_MINB64 : SMNN_SEP2_MINB) pipe_sep2_kernel(PipeL L, int T, int32_t* info) {
+  pdl_trigger();
+  pdl_wait();
   sep2_body<B, S, MS, NR>(L, T, info, blockIdx.x, int(threadIdx.x), int(blockDim.x), smnn_dyn_smem);
 }
 
@@ -703,6 +715,7 @@ __global__ void __launch_bounds__(SMNN_PIPE_NT, sizeof(S) >= 8 ? (BWD ? (NR == 2
   const Tio* sS = smT + opaque(os + f);
   const Tio* gS = smT + opaque(og + f * B);
   S yL[NR][B], yR[NR][B];
+  pdl_wait();  // the inputs are being staged; the separator solution (and P1's state) must be complete
   if (act) {
     const S* ys = reinterpret_cast<const S*>(L.ysep) + g * int64_t(NR * B) * K + k;
 #pragma unroll
