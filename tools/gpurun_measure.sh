@@ -1,5 +1,5 @@
 # GPU box: full round-2 pass -- parity suite, smoke, bench lines, launch list, ncu --set full
-O=gpurun_out/measure5; mkdir -p $O
+O=gpurun_out/measure6; mkdir -p $O
 nvidia-smi --query-gpu=name,driver_version,clocks.max.sm --format=csv,noheader > $O/gpu.txt
 rm -f gpurun_out/parity/errors.jsonl
 timeout 2400 python -m pytest tests -m gpu -q --timeout 1200 --durations=15 -p no:cacheprovider > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log
